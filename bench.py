@@ -1,0 +1,398 @@
+"""bench.py — MoEpic split-expert MoE decode on B200 (BASELINE.json metric / configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config mixtral]
+
+One step = one decode token through the whole L-layer MoE-only stack (every §8(a) row runs per
+layer: routing K1 + fused next-layer predictor, classification / admission, on-demand H2D of
+missing segments, K2 over resident / prefetched / on-demand segments, combine, next-layer
+prefetch).  Workload (configs[1]): Mixtral-8x7B-shaped layers (d 4096, I 14336, 8 experts
+top-2), 32 logical layers, bf16, batch 1, 50 % expert VRAM budget (V_e = 128 experts,
+theta 0.5 -> every top cached), LCP, prefetch of the top-K predicted experts.  Host RAM
+holds L_host physical layers (logical layer i reads physical i mod L_host); every byte still
+crosses PCIe.  Weights are random (synth/), inputs are the seeded
+"organic" routing process.  Expert bytes streamed per layer (~700 MB) exceed L2 (126 MB), so
+no explicit flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  `value` = tokens/s over the timed region (CUDA events,
+max over ranks); `e2e` = same through moepic_layer_forward_host (host buffers, H2D/D2H in the
+timed region); `roofline` = K2 (the dominant kernel) achieved HBM GB/s vs the measured peak;
+`path_roofline` = max(HBM bytes / HBM peak, PCIe bytes / PCIe peak) vs measured time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer decode throughput at 50% expert VRAM budget (tokens/s through the MoE stack)"
+
+CONFIGS = {
+    # name: (shape, L, L_host, B, v_e fraction, theta)
+    "mixtral": dict(shape="mixtral", L=32, L_host=2, B=1, budget=0.5, theta=0.5),
+    "qwen3": dict(shape="qwen3", L=48, L_host=4, B=1, budget=0.5, theta=0.5),
+    "deepseek": dict(shape="deepseek", L=26, L_host=4, B=1, budget=0.5, theta=0.5),
+    "toy": dict(shape="toy", L=2, L_host=2, B=1, budget=0.25, theta=0.5),
+}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def pcie_probe(torch, nbytes=1 << 30, reps=10):
+    """Pinned H2D bandwidth, best of `reps` (SURVEY §8(d) PCIe_peak probe)."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            a.record(s)
+            d.copy_(h, non_blocking=True)
+            b.record(s)
+        b.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del h, d
+    return best
+
+
+def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print):
+    S = synth.SHAPES[cfg["shape"]]
+    L, Lh = cfg["L"], cfg["L_host"]
+    N_local = S.N // world
+    v_e = cfg["budget"] * L * N_local
+    desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=64 if S.I % 64 == 0 else 16,
+                          max_batch=max_batch, renorm_topk=S.renorm, L_host=Lh, v_e_max=v_e,
+                          ep_rank=rank, ep_size=world)
+    t0 = time.time()
+    ctx = api.MoEpic(desc)
+    for i in range(L):
+        ctx.load_router(i, synth.bf16_bits(synth.router_weights(0, i, S.N, S.d)))
+    lo, hi = rank * N_local, (rank + 1) * N_local
+    keep = {}
+    for pl in range(Lh):
+        for e in range(lo, hi):
+            g, u, dn = synth.expert_weights(0, pl, e, S.d, S.I, device="cuda")
+            bits = tuple(synth.bf16_bits(x) for x in (g, u, dn))
+            ctx.load_expert(pl, e, *bits)
+            if pl == 0:
+                keep[e] = bits
+    for i in range(L):
+        for s in range(S.n_shared):
+            g, u, dn = synth.shared_expert_weights(0, i, s, S.d, S.I, device="cuda")
+            ctx.load_expert(i, -1 - s, *(synth.bf16_bits(x) for x in (g, u, dn)))
+    log(f"[bench] model loaded in {time.time() - t0:.1f}s")
+    return ctx, desc, S, v_e, keep
+
+
+def run_ours(args, log):
+    import numpy as np
+    import torch
+    import synth
+    from paper_2509_08342_b200 import api
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    cfg = CONFIGS[args.config]
+    pcie = pcie_probe(torch)
+    log(f"[bench] pinned H2D probe {pcie:.2f} GB/s")
+    ctx, desc, S, v_e, keep = build_model(api, synth, torch, cfg, rank, world, max_batch=cfg["B"], log=log)
+    L, B = cfg["L"], cfg["B"]
+    t0 = time.time()
+    ctx.configure(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
+    log(f"[bench] configure (re-layout {v_e:.0f} tops) {time.time() - t0:.1f}s")
+    T = args.warmup + args.steps
+    H = synth.hidden_states(1, T + args.e2e_steps + 1, L, S.d).to("cuda")  # [T][L][d]
+    y = torch.empty(B, S.d, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()
+    F = api.M.FUSE_PREDICT
+
+    def token(t):
+        for i in range(L):
+            ctx.layer_forward(i, H[t, i][None], y, stream=stream, flags=F, trace=False)
+            if world > 1:
+                pass  # combine: all-reduce of partial y (below, per layer) — see DESIGN.md §EP
+
+    def token_ep(t):
+        for i in range(L):
+            ctx.layer_forward(i, H[t, i][None], y, stream=stream, flags=F, trace=False)
+            with torch.cuda.stream(stream):
+                dist.all_reduce(y)
+
+    step = token_ep if world > 1 else token
+    for t in range(args.warmup):
+        step(t)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    c0 = ctx.counters()
+    ctx.profile(True)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    per_tok = []
+    for t in range(args.warmup, T):
+        a = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step(t)
+        b = torch.cuda.Event(enable_timing=True)
+        b.record(stream)
+        per_tok.append((a, b))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    tok_ms = [a.elapsed_time(b) for a, b in per_tok]
+    if dist:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    c1 = ctx.counters()
+    k2 = ctx.profile_read(api.M.KERNEL_EXPERT)
+    k1 = ctx.profile_read(api.M.KERNEL_ROUTER)
+    k3 = ctx.profile_read(api.M.KERNEL_COMBINE)
+    ctx.profile(False)
+    dc = {k: c1[k] - c0[k] for k in c1}
+    tokens = args.steps * B
+    value = tokens / (ms / 1e3)
+    layer_us = ms * 1e3 / (args.steps * L)
+
+    # ---- end to end through the host-buffer API (pinned staging inside the library)
+    e2e = None
+    if args.e2e_steps > 0:
+        Hh = [[synth.bf16_bits(H[t, i][None].cpu()) for i in range(L)] for t in range(T, T + args.e2e_steps)]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(args.e2e_steps):
+            for i in range(L):
+                yh, _ = ctx.layer_forward_host(i, Hh[t][i], stream=stream, flags=F, trace=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": round(args.e2e_steps * B / (ems / 1e3), 4), "unit": "tokens/s",
+               "h2d_bytes_per_step": L * B * S.d * 2, "d2h_bytes_per_step": L * B * S.d * 4,
+               "api": "moepic_layer_forward_host"}
+
+    peaks = _peaks()
+    hbm_peak = float(peaks["hbm_gbs"])
+    k2_gbs = k2["bytes"] / (k2["total_ms"] * 1e-3) / 1e9 if k2["total_ms"] > 0 else 0.0
+    pcie_moved = dc["pcie_ondemand_bytes"] + dc["pcie_prefetch_bytes"]
+    t_roof = max(dc["hbm_bytes"] / (hbm_peak * 1e9), pcie_moved / (pcie * 1e9))
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded random weights, organic routing process; synth/)",
+        "config": {"workload": f"{args.config}-shaped decode, B={B}, {cfg['budget']:.0%} expert VRAM budget",
+                   "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
+                   "global_batch": B, "seq_len": 1, "parallelism": f"ep{world}" if world > 1 else "single",
+                   "v_e_experts": v_e, "theta": cfg["theta"], "policy": "LCP", "y_cap": S.K * B,
+                   "l2": "inputs larger than L2 (>=700 MB of expert rows streamed per layer)"},
+        "layer_latency_us": {"mean": round(layer_us, 2),
+                             "p50_token_ms": round(statistics.median(tok_ms), 3),
+                             "p95_token_ms": round(sorted(tok_ms)[max(0, math.ceil(0.95 * len(tok_ms)) - 1)], 3)},
+        "gpu_launches": int(dc["kernel_launches"]),
+        "roofline": {"bound": "hbm", "kernel": "k2_split_expert", "achieved": round(k2_gbs, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(k2_gbs / hbm_peak, 4), "traffic": None,
+                     "launches": k2["launches"], "avg_launch_us": round(k2["total_ms"] * 1e3 / max(1, k2["launches"]), 2),
+                     "bytes_per_launch": int(k2["bytes"] / max(1, k2["launches"])),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
+        "path_roofline": {"bound": "pcie" if pcie_moved / pcie > dc["hbm_bytes"] / hbm_peak else "hbm",
+                          "pcie_peak_gbs": round(pcie, 2), "pcie_nominal_gbs": 63.0,
+                          "pcie_bytes_moved": pcie_moved, "pcie_ondemand_bytes": dc["pcie_ondemand_bytes"],
+                          "pcie_prefetch_bytes": dc["pcie_prefetch_bytes"], "hbm_bytes": dc["hbm_bytes"],
+                          "roofline_ms": round(t_roof * 1e3, 3), "measured_ms": round(ms, 3),
+                          "frac": round(t_roof * 1e3 / ms, 4),
+                          "achieved_pcie_gbs": round(pcie_moved / (ms * 1e-3) / 1e9, 2)},
+        "kernels_ms": {"router": round(k1["total_ms"], 3), "expert": round(k2["total_ms"], 3),
+                       "combine": round(k3["total_ms"], 3)},
+        "cache": {"alpha": dc["act_alpha"], "beta": dc["act_beta"], "gamma": dc["act_gamma"],
+                  "pred_hit_rate": round(dc["pred_hits"] / max(1, dc["pred_total"]), 4)},
+        "clocks": ck, "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(keep, S, cfg, args, log)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+    return out if rank == 0 else None
+
+
+def _oracle_layer_step(S, cfg, keep_bits, h_bits, router_bits):
+    from oracle import numeric as ON
+    return ON.moe_layer(h_bits, router_bits, lambda e: keep_bits[e], S.K)
+
+
+def cpu_baseline(keep, S, cfg, args, log, n_layer_steps=3):
+    """The fp64 oracle as it stands on the host cores: n_layer_steps single-token layer steps of
+    the same workload, extrapolated to tokens/s through L layers."""
+    import numpy as np
+    import synth
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    router = synth.bf16_bits(synth.router_weights(0, 0, S.N, S.d))
+    H = synth.hidden_states(1, n_layer_steps, 1, S.d)
+    missing = [e for e in range(S.N) if e not in keep]
+    if missing:
+        return None
+    ts = []
+    for t in range(n_layer_steps):
+        hb = synth.bf16_bits(H[t, 0][None])
+        t0 = time.perf_counter()
+        _oracle_layer_step(S, cfg, keep, hb, router)
+        ts.append(time.perf_counter() - t0)
+    per_layer = statistics.mean(ts)
+    return {"value": round(1.0 / (per_layer * cfg["L"]), 6), "unit": "tokens/s", "cores": cores,
+            "kind": "oracle", "sample": f"{n_layer_steps} single-token layer steps of layer 0 (fp64 numpy), "
+                                        f"{per_layer * 1e3:.0f} ms each, extrapolated x{cfg['L']} layers",
+            "cpu": _cpu_name()}
+
+
+def _cpu_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, log):
+    """--impl reference: the oracle (fp64 CPU) on this config, each step one single-token layer
+    step of layer 0 (bounded sample), value extrapolated to tokens/s through L layers."""
+    import numpy as np
+    import torch
+    import synth
+    cfg = CONFIGS[args.config]
+    S = synth.SHAPES[cfg["shape"]]
+    keep = {}
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    for e in range(S.N):
+        keep[e] = tuple(synth.bf16_bits(x) for x in synth.expert_weights(0, 0, e, S.d, S.I, device=dev))
+    router = synth.bf16_bits(synth.router_weights(0, 0, S.N, S.d))
+    H = synth.hidden_states(1, args.warmup + args.steps, 1, S.d)
+    for t in range(args.warmup):
+        _oracle_layer_step(S, cfg, keep, synth.bf16_bits(H[t, 0][None]), router)
+    t0 = time.perf_counter()
+    for t in range(args.warmup, args.warmup + args.steps):
+        _oracle_layer_step(S, cfg, keep, synth.bf16_bits(H[t, 0][None]), router)
+    dt = time.perf_counter() - t0
+    per_layer = dt / args.steps
+    value = 1.0 / (per_layer * cfg["L"])
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "tokens/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_layer * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random weights)",
+            "config": {"workload": f"{args.config}-shaped decode, B=1, one layer step per bench step",
+                       "layers_extrapolated": cfg["L"]},
+            "cpu_baseline": {"value": round(value, 6), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} single-token layer steps (layer 0), x{cfg['L']} layers",
+                             "cpu": _cpu_name()},
+            "e2e": {"value": round(value, 6), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, log)), flush=True)
+        return
+    out = run_ours(args, log)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

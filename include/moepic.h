@@ -1,0 +1,219 @@
+/* moepic.h — C ABI of the B200-native MoEpic split-expert MoE layer library.
+ *
+ * MoEpic (arXiv 2509.08342, "Accelerating Mixture-of-Expert Inference with Adaptive Expert
+ * Split Mechanism").  Citations "P:<n>" are lines of the paper text; readings of
+ * silent or ambiguous passages are numbered Q1..Q26 in DESIGN.md.
+ *
+ * What one library context does:
+ *   - every expert of every layer lives in pinned host RAM in a row-interleaved layout
+ *     (row r = [gate_r | up_r | down[:, r]], 6*d bytes);
+ *   - each expert is split along its intermediate dimension I at I_top rows (reading Q1/Q2);
+ *     the TOP rows of the C_i hottest experts of layer i stay cached in HBM;
+ *   - layer_forward routes the batch (top-K gate softmax), computes the resident
+ *     segments at once, streams missing bottoms / experts over PCIe on a copy stream and
+ *     computes them when they land, sums the partial down-projections;
+ *   - the same call runs the NEXT layer's router on the current activation (Eq. 3)
+ *     and prefetches that layer's bottoms (or full experts) in descending predicted score
+ *      into a ping-pong HBM buffer of U_b expert units;
+ *   - a host cache manager (LCP Eq. 4 / LRU / LFU / RND) admits missed experts;
+ *   - configure runs Alg. 1 on the recorded statistics and re-lays out the cache.
+ *
+ * Conventions for every function:
+ *   - returns moepic_status; nothing throws across the ABI; on a non-OK status
+ *     moepic_last_error(ctx) names the offending argument or the failing CUDA call.
+ *   - MOEPIC_EINVAL leaves the context unchanged.  MOEPIC_ERUNTIME (a CUDA failure) poisons
+ *     the context: every later call returns MOEPIC_ESTATE.
+ *   - "device pointer" = CUDA global memory of the context's device; "host pointer" = plain
+ *     process memory (pageable is fine; it is copied).
+ *   - bf16 values are passed as uint16_t bit patterns.
+ *   - calls on one context must be serialised by the caller (one ctx per process and GPU).
+ */
+#ifndef MOEPIC_H
+#define MOEPIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOEPIC_OK = 0,
+  MOEPIC_EINVAL = 1,   /* bad argument or configuration; context unchanged            */
+  MOEPIC_ERUNTIME = 2, /* a CUDA call failed; context poisoned                           */
+  MOEPIC_ENOMEM = 3,   /* the arena (or pinned host memory) is too small                 */
+  MOEPIC_ESTATE = 4    /* context poisoned by an earlier MOEPIC_ERUNTIME                 */
+} moepic_status;
+
+/* cache replacement policy (Table 1) */
+typedef enum { MOEPIC_LCP = 0, MOEPIC_LRU = 1, MOEPIC_LFU = 2, MOEPIC_RND = 3 } moepic_policy;
+
+/* activation classes: all rows resident / top only / nothing resident */
+enum { MOEPIC_ALPHA = 0, MOEPIC_BETA = 1, MOEPIC_GAMMA = 2 };
+/* admission victim codes in moepic_trace.adm_victim */
+enum { MOEPIC_ADM_FREE_SLOT = -1, MOEPIC_ADM_NONE = -2 };
+
+/* layer_forward flags */
+enum {
+  MOEPIC_FUSE_PREDICT = 1, /* run R^{(i+1) mod L} on h^i and prefetch that layer (Eq. 3)    */
+  MOEPIC_RESIDUAL = 2      /* y = h + MoE(h) instead of MoE(h) (Eq. 2's inner h + sum) */
+};
+
+typedef struct moepic_ctx moepic_ctx;
+
+/* Model shape (Table 2).  Invariants (EINVAL otherwise):
+ *   1 <= K < N; L >= 1; d % 8 == 0 and d >= 8; I % row_granule == 0;
+ *   row_granule % 16 == 0; buffer_experts >= K (U_b); 1 <= max_batch <= 4096;
+ *   1 <= L_host <= L; 0 <= ep_rank < ep_size; N % ep_size == 0.                               */
+typedef struct {
+  int32_t L, N, K, d, I;  /* layers, routed experts per layer, top-K, hidden, intermediate     */
+  int32_t n_shared;       /* shared experts per layer: always resident, weight 1, unsplit (Q6) */
+  int32_t row_granule;    /* g: I_top is a multiple of g (reading Q2); default 64              */
+  int32_t buffer_experts; /* U_b in full-expert units per ping-pong half (default K)      */
+  int32_t max_batch;      /* largest B passed to layer_forward / predict_prefetch              */
+  int32_t renorm_topk;    /* 1: Eq. 2 renormalised gate (default); 0: raw softmax s_j (Q4)      */
+  int32_t L_host;         /* distinct layers stored in pinned host RAM; logical layer i reads
+                             physical layer i % L_host (bench aliasing)             */
+  double v_e_max;         /* largest expert-cache budget V_e (full-expert units) configure may
+                             request; sizes the HBM slot pool                                  */
+  int32_t ep_rank, ep_size; /* expert parallel: expert e is local iff e*ep_size/N == ep_rank   */
+} moepic_model_desc;
+
+/* Cache configuration.  EINVAL when: v_e < 0 or
+ * v_e > v_e_max; any theta_i outside (0, 1]; any v_i < 0; sum v_i > v_e (+1e-9); policy out
+ * of range; rho outside (0,1); omega < 1; zeta outside (0,1); use_solver with an empty
+ * statistics accumulator on some layer; t_load_exp <= 0 or t_moe <= 0 with use_solver. */
+typedef struct {
+  double v_e;              /* V_e: expert-cache budget in full-expert units             */
+  const double* v_i;       /* [L] per-layer budgets, or NULL -> uniform V_e / L         */
+  const double* theta_i;   /* [L] split ratios in (0,1], or NULL -> 0.5; ignored when
+                              use_solver = 1                                                    */
+  int32_t use_solver;      /* 1: run Alg. 1 VramAllocation on the recorded stats        */
+  int32_t policy;          /* moepic_policy                                                     */
+  double rho;              /* LCP rho (default 0.25)                                     */
+  int32_t omega;           /* LCP omega (default 128)                                    */
+  double zeta;             /* allocation granularity (default 0.01)                      */
+  double t_att, t_moe, t_head, t_load_exp; /* profiled latencies, any one time unit   */
+  const int32_t* y_cap_i;  /* [L] max prefetch count per layer, or NULL (buffer-bound)          */
+  int32_t prefetch;        /* 0: no speculative prefetch (cache-only baseline); 1: on          */
+  uint64_t seed;           /* splitmix64 seed: initial random cached set, RND victims   */
+} moepic_cache_config;
+
+/* configure output: caller-owned arrays of length L (any may be NULL) */
+typedef struct {
+  int32_t* C_i;        /* cache size (experts whose top is cached)                            */
+  int32_t* I_top_i;    /* rows per cached top segment = g*floor(theta_i*I/g + 1e-9) (Q2)      */
+  double* theta_eff_i; /* I_top_i / I                                                          */
+  double* V_i;         /* budget per layer after Alg. 1                                        */
+} moepic_config_out;
+
+/* Per-call trace; every array is caller-owned and may be NULL (then it is not written).
+ * Capacities: ids/w >= B*K; act_* , adm_*, plan_* >= N.                                       */
+typedef struct {
+  int32_t* ids;           /* [B*K] routed experts per token in key order (l desc, id asc)    */
+  float* w;               /* [B*K] gate weights (Eq. 2)                                       */
+  int32_t* act_expert;    /* distinct activated experts, order (B_e desc, id asc)  (Q9)      */
+  int8_t* act_class;      /* MOEPIC_ALPHA / BETA / GAMMA, state before the call      */
+  int32_t n_act;
+  int32_t* adm_expert;    /* cache admissions in order (Q11)                           */
+  int32_t* adm_victim;    /* evicted expert, or MOEPIC_ADM_FREE_SLOT / MOEPIC_ADM_NONE       */
+  int32_t n_adm;
+  int32_t* plan_expert;   /* prefetch plan made by this call for the next layer  */
+  int8_t* plan_full;      /* 1 = full expert, 0 = bottom segment only                 */
+  int32_t n_plan;
+  int32_t plan_layer;     /* layer the plan targets, -1 if none                               */
+  uint64_t pcie_ondemand_bytes; /* H2D bytes of missing segments of this layer        */
+  uint64_t pcie_prefetch_bytes; /* H2D bytes of the plan issued by this call                  */
+  uint64_t hbm_bytes;     /* algorithmic HBM bytes of this call          */
+  int32_t kernel_launches;/* kernels this call enqueued                                       */
+  int32_t* ranking;       /* [N] predicted ranking R' the plan was built from (Eq. 3, Q9)    */
+} moepic_trace;
+
+/* Bytes of device memory moepic_create needs for this model (slot pool for v_e_max, two
+ * ping-pong buffers, routers, shared experts, workspace).  Host-only; no CUDA call.            */
+moepic_status moepic_arena_bytes(const moepic_model_desc* desc, size_t* bytes);
+
+/* Create a context on the current CUDA device.  dev_arena: caller-owned device allocation of
+ * >= moepic_arena_bytes bytes, 256-byte aligned, that outlives the context.  The context
+ * allocates pinned host memory for L_host*N experts (+ a mapped mailbox), a copy stream and
+ * events.  On success *out is a new context; on failure *out is NULL.                         */
+moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size_t dev_bytes,
+                            moepic_ctx** out);
+
+/* Router R^layer: w_bf16 host pointer to [N][d] bf16 (row j = expert j), copied.  layer < L. */
+moepic_status moepic_load_router(moepic_ctx* ctx, int32_t layer, const uint16_t* w_bf16);
+
+/* Expert weights in HuggingFace layout, host pointers, copied into the pinned arena in the
+ * row-interleaved layout: gate [I][d], up [I][d], down [d][I] (bf16).  layer < L_host for
+ * routed experts (expert in [0,N)); shared expert s is expert = -1 - s with layer < L.        */
+moepic_status moepic_load_expert(moepic_ctx* ctx, int32_t layer, int32_t expert,
+                                 const uint16_t* gate, const uint16_t* up, const uint16_t* down);
+
+/* Blocking ("when the device is idle"): synchronises the device, computes
+ * {V_i, theta_i, C_i} (uniform/given, or Alg. 1 when use_solver), ranks experts by cache
+ * priority and copies the top segments of the top-C_i experts into HBM; drops
+ * any pending prefetch.  out may be NULL.                                                      */
+moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg,
+                               moepic_config_out* out);
+
+/* One MoE layer over a batch.
+ *   h_dev: device pointer, bf16 [B][d] row-major (h^i);  1 <= B <= max_batch.
+ *   y_dev: device pointer, fp32 [B][d] (written; Eq. 2 inner sum, + h if MOEPIC_RESIDUAL).
+ *   stream: cudaStream_t (as void*; NULL = legacy default stream) all compute is ordered on.
+ *   trace: may be NULL.
+ * Blocks the host only until the routing of this batch is known (it plans copies); returns
+ * with the GPU work enqueued on `stream`.  y_dev is valid after the stream reaches it.        */
+moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B,
+                                   float* y_dev, void* stream, uint32_t flags,
+                                   moepic_trace* trace);
+
+/* Same as moepic_layer_forward with HOST buffers: h_host bf16 [B][d] is copied to the device,
+ * y_host fp32 [B][d] is written before return (the call synchronises `stream`).               */
+moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const uint16_t* h_host,
+                                        int32_t B, float* y_host, void* stream, uint32_t flags,
+                                        moepic_trace* trace);
+
+/* Speculative prefetch for layer next_layer from activation h_dev (bf16 [B][d], device):
+ * runs R^{next_layer}(h) (Eq. 3), ranks experts (Q9) and issues the prefetch plan.
+ * Used for layer 0 with the previous token's last activation (Q23).  Replaces any
+ * pending plan.  trace (plan fields only) may be NULL.                                         */
+moepic_status moepic_predict_prefetch(moepic_ctx* ctx, int32_t next_layer, const void* h_dev,
+                                      int32_t B, void* stream, moepic_trace* trace);
+
+/* Statistics snapshot (checkpoint / offline configurator experiments).  buf == NULL queries the
+ * size into *bytes; otherwise writes at most *bytes bytes.  set_stats restores a snapshot taken
+ * from a context with the same (L, N, K).                                                      */
+moepic_status moepic_get_stats(moepic_ctx* ctx, void* buf, size_t* bytes);
+moepic_status moepic_set_stats(moepic_ctx* ctx, const void* buf, size_t bytes);
+
+/* Cumulative counters since create. */
+typedef struct {
+  uint64_t layer_steps, kernel_launches, h2d_copies;
+  uint64_t pcie_ondemand_bytes, pcie_prefetch_bytes, hbm_bytes;
+  uint64_t act_alpha, act_beta, act_gamma;    /* class counts over all steps                  */
+  uint64_t pred_hits, pred_total;             /* activated experts that were planned / total  */
+} moepic_counters;
+moepic_status moepic_get_counters(moepic_ctx* ctx, moepic_counters* out);
+
+/* Kernel timing with CUDA events recorded on the launching stream around every launch of the
+ * given kernel class while profiling is enabled.  bytes = algorithmic HBM bytes of those
+ * launches (K2: weight rows x 6d + activations).                          */
+typedef struct {
+  uint64_t launches;
+  double total_ms;
+  uint64_t bytes;
+} moepic_kernel_stats;
+enum { MOEPIC_KERNEL_ROUTER = 0, MOEPIC_KERNEL_EXPERT = 1, MOEPIC_KERNEL_COMBINE = 2 };
+/* enable != 0 starts (and resets) event timing; 0 stops it.                                   */
+moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable);
+/* Synchronises the recorded events and returns the totals for one kernel class.               */
+moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_kernel_stats* out);
+
+const char* moepic_last_error(const moepic_ctx* ctx);   /* never NULL; "" when none           */
+void moepic_destroy(moepic_ctx* ctx);                    /* NULL is a no-op; syncs the device  */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEPIC_H */

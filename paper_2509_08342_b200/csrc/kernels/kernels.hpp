@@ -1,0 +1,86 @@
+// Internal launch interface of the MoEpic sm_100a kernels (not part of the C ABI).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifdef __CUDACC__
+#define MOEPIC_HD __host__ __device__
+#else
+#define MOEPIC_HD
+#endif
+
+namespace moepic {
+
+constexpr int kMaxN = 512;          // routed experts per layer supported by K1
+constexpr int kK2Threads = 256;
+constexpr int kK2Stages = 4;
+constexpr int kMaxLaunchSegs = 256; // segments per K2 launch (kernel-parameter array)
+constexpr int kMaxStepSegs = 1024;  // segments per combine launch
+
+// ------------------------------------------------------------------ K1: router + predictor
+struct RouterParams {
+  const uint16_t* h;      // [B][d] bf16
+  const uint16_t* W0;     // R^i [N][d] (routing) or nullptr
+  const uint16_t* W1;     // R^j [N][d] (prediction) or nullptr
+  double* logits;         // [2][B][N] scratch
+  int32_t* ids;           // [B][K] out
+  float* w;               // [B][K] out
+  int32_t* ranking;       // [N] out
+  unsigned int* ticket;   // zero-initialised, reset by the kernel
+  // mapped pinned mailbox (device aliases)
+  int32_t* mb_ids;
+  float* mb_w;
+  int32_t* mb_rank;
+  volatile uint32_t* mb_seq;
+  uint32_t seq;
+  int B, d, N, K, renorm;
+};
+void launch_router(const RouterParams& p, cudaStream_t s);
+
+// ------------------------------------------------------------------ K2: split-expert stream
+struct Seg {
+  const uint8_t* base;    // first row of the segment (row-interleaved layout, 6d bytes/row)
+  int32_t expert;         // routed expert id, or -1 - s for shared expert s (weight 1)
+  int32_t nrows;
+  uint32_t tok_mask;      // tokens (bits) this segment serves; popcount <= kMaxTB
+  int32_t row_begin;      // prefix of rows in this launch
+  int64_t ws_off;         // float offset of the segment's partial area in the workspace
+  int32_t cta_first;      // first CTA whose row range overlaps this segment
+  int32_t pad;
+};
+
+struct K2Params {
+  const uint16_t* h;      // [B][d]
+  const int32_t* ids;     // [B][K]
+  const float* w;         // [B][K]
+  float* ws;              // partial sums
+  int64_t total_rows;
+  int d, K, nsegs;
+  Seg segs[kMaxLaunchSegs];
+};
+// Partition rule shared with the host: CTA c of G owns launch rows [c*R/G, (c+1)*R/G).
+MOEPIC_HD inline int64_t k2_row_lo(int64_t c, int64_t R, int64_t G) { return c * R / G; }
+int k2_rows_per_tile(int d);
+int k2_max_tokens(int d);
+size_t k2_smem_bytes(int d);
+void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s);
+
+// ------------------------------------------------------------------ K3: combine
+struct CombineSeg {
+  int64_t ws_off;
+  int32_t nchunks;
+  uint32_t tok_mask;
+};
+struct CombineParams {
+  float* y;               // [B][d] fp32 out
+  const uint16_t* h;      // residual source
+  const float* ws;
+  int B, d, residual, nsegs;
+  CombineSeg segs[kMaxStepSegs];
+};
+void launch_combine(const CombineParams& p, cudaStream_t s);
+
+bool kernels_init(char* err, size_t errlen);  // sets smem attributes; returns false on failure
+
+}  // namespace moepic

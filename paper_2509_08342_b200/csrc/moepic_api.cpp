@@ -1,0 +1,1029 @@
+// C ABI of the MoEpic library (include/moepic.h, include/moepic_hostsim.h).
+//
+// One context = one GPU: the host control plane (host/control.hpp), the device arena layout,
+// the copy stream ("transfer engine"), the mapped-pinned routing mailbox and the kernel
+// launches of one MoE layer step:
+//   K1 router (+ next-layer predictor) -> host waits on the mailbox -> control-plane step
+//   -> on-demand H2D copies of missing segments (copy stream) -> K2 over resident tops (no
+//   wait) -> K2 over prefetched segments (wait plan event) -> K2 over on-demand segments
+//   (wait copy event) -> K3 combine -> next-layer prefetch plan issued on the copy stream.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/moepic.h"
+#include "../../include/moepic_hostsim.h"
+#include "host/control.hpp"
+#include "kernels/kernels.hpp"
+
+using namespace moepic;
+
+namespace {
+
+constexpr int kSMs = 148;
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+struct ArenaLayout {
+  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, total;
+  uint64_t pool_rows, plan_rows, od_rows, ws_floats;
+};
+
+int n_local(const moepic_model_desc& d) { return d.N / d.ep_size; }
+
+std::string validate_desc(const moepic_model_desc* d) {
+  if (!d) return "desc is NULL";
+  if (d->L < 1) return "L must be >= 1";
+  if (d->N < 2 || d->N > kMaxN) return "N must be in [2, 512]";
+  if (d->K < 1 || d->K >= d->N) return "K must be < N";
+  if (d->K > 64) return "K must be <= 64";
+  if (d->d < 8 || d->d % 8 != 0 || d->d > 4096) return "d must be a multiple of 8 in [8, 4096]";
+  if (d->row_granule < 16 || d->row_granule % 16 != 0) return "row_granule must be a positive multiple of 16";
+  if (d->I < d->row_granule || d->I % d->row_granule != 0) return "I must be a multiple of row_granule";
+  if (d->n_shared < 0 || d->n_shared > 8) return "n_shared must be in [0, 8]";
+  if (d->buffer_experts < d->K) return "buffer_experts must be >= K";
+  if (d->max_batch < 1 || d->max_batch > 32) return "max_batch must be in [1, 32]";
+  if (d->L_host < 1 || d->L_host > d->L) return "L_host must be in [1, L]";
+  if (!(d->v_e_max >= 0.0)) return "v_e_max must be >= 0";
+  if (d->ep_size < 1 || d->ep_rank < 0 || d->ep_rank >= d->ep_size) return "ep_rank / ep_size invalid";
+  if (d->N % d->ep_size != 0) return "N must be divisible by ep_size";
+  return "";
+}
+
+ArenaLayout arena_layout(const moepic_model_desc& d) {
+  ArenaLayout a{};
+  const uint64_t rb = 6ull * d.d;
+  const int Nl = n_local(d);
+  size_t off = 0;
+  a.routers = off; off = align_up(off + (size_t)d.L * d.N * d.d * 2);
+  a.shared = off; off = align_up(off + (size_t)d.L * d.n_shared * d.I * rb);
+  a.pool_rows = (uint64_t)std::ceil(d.v_e_max * (double)d.I - 1e-9);
+  a.pool = off; off = align_up(off + a.pool_rows * rb);
+  a.plan_rows = (uint64_t)d.buffer_experts * d.I;
+  a.od_rows = (uint64_t)std::min(Nl, d.max_batch * d.K) * d.I;
+  for (int i = 0; i < 2; ++i) { a.buf[i] = off; off = align_up(off + (a.plan_rows + a.od_rows) * rb); }
+  a.ws_floats = (uint64_t)d.d * (4ull * (d.max_batch * d.K + d.n_shared * d.max_batch) + 3ull * (kSMs + 1) * 8 + 64);
+  a.ws = off; off = align_up(off + a.ws_floats * 4);
+  a.logits = off; off = align_up(off + (size_t)2 * d.max_batch * d.N * 8);
+  a.ids = off; off = align_up(off + (size_t)d.max_batch * d.K * 4);
+  a.w = off; off = align_up(off + (size_t)d.max_batch * d.K * 4);
+  a.ranking = off; off = align_up(off + (size_t)d.N * 4);
+  a.ticket = off; off = align_up(off + 64);
+  a.total = off;
+  return a;
+}
+
+moepic_status fail(std::string* err, moepic_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (err) *err = buf;
+  return st;
+}
+
+CacheParams to_params(const moepic_cache_config* c, int L) {
+  CacheParams p;
+  p.v_e = c->v_e;
+  if (c->v_i) p.v_i.assign(c->v_i, c->v_i + L);
+  if (c->theta_i) p.theta_i.assign(c->theta_i, c->theta_i + L);
+  p.use_solver = c->use_solver != 0;
+  p.policy = c->policy;
+  p.rho = c->rho;
+  p.omega = c->omega;
+  p.zeta = c->zeta;
+  p.t_att = c->t_att; p.t_moe = c->t_moe; p.t_head = c->t_head; p.t_load = c->t_load_exp;
+  if (c->y_cap_i) p.y_cap.assign(c->y_cap_i, c->y_cap_i + L);
+  p.prefetch = c->prefetch != 0;
+  p.seed = c->seed;
+  return p;
+}
+
+void write_config_out(const ControlPlane& cp, moepic_config_out* out) {
+  if (!out) return;
+  for (int i = 0; i < cp.L; ++i) {
+    const LayerState& l = cp.layers[i];
+    if (out->C_i) out->C_i[i] = l.C;
+    if (out->I_top_i) out->I_top_i[i] = l.I_top;
+    if (out->theta_eff_i) out->theta_eff_i[i] = (double)l.I_top / (double)cp.I;
+    if (out->V_i) out->V_i[i] = l.V;
+  }
+}
+
+uint64_t step_hbm_bytes(const ControlPlane& cp, const StepResult& r, int B, int n_router,
+                        uint64_t prefetch_bytes) {
+  const uint64_t rb = (uint64_t)cp.row_bytes;
+  return (uint64_t)r.A.size() * cp.I * rb + (uint64_t)cp.n_shared * cp.I * rb +
+         (uint64_t)n_router * cp.N * cp.d * 2 + (uint64_t)B * cp.d * 2 + (uint64_t)B * cp.d * 4 + r.d2d_bytes +
+         r.pcie_ondemand + prefetch_bytes;
+}
+
+void fill_step_trace(moepic_trace* tr, const StepResult& r, const Plan* next) {
+  if (!tr) return;
+  tr->n_act = (int32_t)r.A.size();
+  for (size_t a = 0; a < r.A.size(); ++a) {
+    if (tr->act_expert) tr->act_expert[a] = r.A[a];
+    if (tr->act_class) tr->act_class[a] = r.cls[a];
+  }
+  tr->n_adm = (int32_t)r.adm.size();
+  for (size_t a = 0; a < r.adm.size(); ++a) {
+    if (tr->adm_expert) tr->adm_expert[a] = r.adm[a].expert;
+    if (tr->adm_victim) tr->adm_victim[a] = r.adm[a].victim;
+  }
+  tr->n_plan = 0;
+  tr->plan_layer = -1;
+  tr->pcie_prefetch_bytes = 0;
+  if (next && next->valid) {
+    tr->plan_layer = next->target;
+    tr->n_plan = (int32_t)next->items.size();
+    if (tr->ranking)
+      for (size_t k = 0; k < next->ranking.size(); ++k) tr->ranking[k] = next->ranking[k];
+    for (size_t k = 0; k < next->items.size(); ++k) {
+      if (tr->plan_expert) tr->plan_expert[k] = next->items[k].expert;
+      if (tr->plan_full) tr->plan_full[k] = next->items[k].full ? 1 : 0;
+    }
+  }
+  tr->pcie_ondemand_bytes = r.pcie_ondemand;
+}
+
+uint64_t plan_bytes(const Plan& p, int64_t rb) {
+  uint64_t s = 0;
+  for (auto& it : p.items) s += (uint64_t)it.rows * (uint64_t)rb;
+  return s;
+}
+
+}  // namespace
+
+// ====================================================================== context
+struct moepic_ctx {
+  moepic_model_desc desc{};
+  ArenaLayout lay{};
+  std::unique_ptr<ControlPlane> cp;
+  uint8_t* arena = nullptr;
+  uint8_t* host_experts = nullptr;   // pinned [L_host][N_local][I][6d]
+  uint8_t* mailbox = nullptr;        // mapped pinned
+  uint8_t* mailbox_dev = nullptr;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_od = nullptr, ev_plan[2] = {nullptr, nullptr}, ev_step[2] = {nullptr, nullptr};
+  bool ev_step_rec[2] = {false, false};
+  cudaEvent_t ev_tmp = nullptr;
+  std::vector<uint64_t> slot_base;   // per layer: byte offset inside the pool
+  bool configured = false;
+  Plan pending;
+  int last_buf = 1;
+  uint32_t seq = 0;
+  bool poisoned = false;
+  std::string err;
+  moepic_counters ctr{};
+  // event profiling (moepic_profile): pairs recorded on the launching stream
+  struct ProfEv {
+    cudaEvent_t a, b;
+    int cls;
+    uint64_t bytes;
+  };
+  bool profiling = false;
+  std::vector<ProfEv> prof;
+  size_t prof_used = 0;
+  moepic_kernel_stats prof_acc[3]{};
+
+  int prof_begin(cudaStream_t s, int cls) {
+    if (!profiling) return -1;
+    if (prof_used == prof.size()) {
+      ProfEv e{};
+      if (cudaEventCreate(&e.a) != cudaSuccess || cudaEventCreate(&e.b) != cudaSuccess) return -1;
+      prof.push_back(e);
+    }
+    ProfEv& e = prof[prof_used];
+    e.cls = cls;
+    e.bytes = 0;
+    if (cudaEventRecord(e.a, s) != cudaSuccess) return -1;
+    return (int)prof_used++;
+  }
+  void prof_end(int idx, cudaStream_t s, uint64_t bytes) {
+    if (idx < 0) return;
+    prof[idx].bytes = bytes;
+    cudaEventRecord(prof[idx].b, s);
+    if (prof_used >= 4096) prof_drain();
+  }
+  void prof_drain() {
+    for (size_t i = 0; i < prof_used; ++i) {
+      float ms = 0.f;
+      cudaEventSynchronize(prof[i].b);
+      cudaEventElapsedTime(&ms, prof[i].a, prof[i].b);
+      moepic_kernel_stats& k = prof_acc[prof[i].cls];
+      k.launches++;
+      k.total_ms += ms;
+      k.bytes += prof[i].bytes;
+    }
+    prof_used = 0;
+  }
+  std::vector<int32_t> ids_h, rank_h;
+  std::vector<float> w_h;
+  uint8_t* scratch_h = nullptr;      // pinned staging for *_host calls
+  size_t scratch_bytes = 0;
+  void* dev_stage = nullptr;         // device staging for *_host calls
+  size_t dev_stage_bytes = 0;
+
+  uint64_t rb() const { return 6ull * desc.d; }
+  int Nl() const { return n_local(desc); }
+  int first_local() const { return desc.ep_rank * Nl(); }
+  const uint8_t* host_expert(int layer, int e) const {
+    const int pl = layer % desc.L_host;
+    return host_experts + ((uint64_t)pl * Nl() + (e - first_local())) * desc.I * rb();
+  }
+  uint8_t* slot_ptr(int layer, int slot) const {
+    return arena + lay.pool + slot_base[layer] + (uint64_t)slot * cp->layers[layer].I_top * rb();
+  }
+  uint8_t* plan_ptr(int buf, int64_t row) const { return arena + lay.buf[buf] + (uint64_t)row * rb(); }
+  uint8_t* od_ptr(int buf, int64_t row) const {
+    return arena + lay.buf[buf] + (lay.plan_rows + (uint64_t)row) * rb();
+  }
+  uint8_t* shared_ptr(int layer, int s) const {
+    return arena + lay.shared + ((uint64_t)layer * desc.n_shared + s) * desc.I * rb();
+  }
+  const uint16_t* router(int layer) const {
+    return reinterpret_cast<const uint16_t*>(arena + lay.routers) + (size_t)layer * desc.N * desc.d;
+  }
+};
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      ctx->poisoned = true;                                                                \
+      return fail(&ctx->err, MOEPIC_ERUNTIME, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                     \
+    }                                                                                      \
+  } while (0)
+
+#define CTX_GUARD()                                                     \
+  do {                                                                  \
+    if (!ctx) return MOEPIC_EINVAL;                                     \
+    if (ctx->poisoned) return MOEPIC_ESTATE;                            \
+  } while (0)
+
+extern "C" {
+
+moepic_status moepic_arena_bytes(const moepic_model_desc* desc, size_t* bytes) {
+  if (!bytes || !validate_desc(desc).empty()) return MOEPIC_EINVAL;
+  *bytes = arena_layout(*desc).total;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size_t dev_bytes,
+                            moepic_ctx** out) {
+  if (!out) return MOEPIC_EINVAL;
+  *out = nullptr;
+  if (!validate_desc(desc).empty()) return MOEPIC_EINVAL;
+  if (!dev_arena || (reinterpret_cast<uintptr_t>(dev_arena) % kAlign) != 0) return MOEPIC_EINVAL;
+  ArenaLayout lay = arena_layout(*desc);
+  if (dev_bytes < lay.total) return MOEPIC_ENOMEM;
+  auto* ctx = new (std::nothrow) moepic_ctx();
+  if (!ctx) return MOEPIC_ENOMEM;
+  ctx->desc = *desc;
+  ctx->lay = lay;
+  ctx->arena = static_cast<uint8_t*>(dev_arena);
+  ctx->cp.reset(new ControlPlane(desc->L, desc->N, desc->K, desc->d, desc->I, desc->row_granule,
+                                 desc->buffer_experts, desc->n_shared, desc->ep_rank, desc->ep_size));
+  char kerr[256];
+  auto bail = [&](moepic_status st) {
+    moepic_destroy(ctx);
+    return st;
+  };
+  if (!kernels_init(kerr, sizeof kerr)) return bail(MOEPIC_ERUNTIME);
+  const uint64_t host_bytes = (uint64_t)desc->L_host * ctx->Nl() * desc->I * ctx->rb();
+  if (cudaHostAlloc(&ctx->host_experts, host_bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(MOEPIC_ENOMEM);
+  }
+  const size_t mb_bytes = 64 + (size_t)desc->max_batch * desc->K * 8 + (size_t)desc->N * 4;
+  if (cudaHostAlloc(&ctx->mailbox, mb_bytes, cudaHostAllocMapped) != cudaSuccess) return bail(MOEPIC_ENOMEM);
+  memset(ctx->mailbox, 0, mb_bytes);
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->mailbox_dev), ctx->mailbox, 0) != cudaSuccess)
+    return bail(MOEPIC_ERUNTIME);
+  if (cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
+  cudaEvent_t* evs[] = {&ctx->ev_od, &ctx->ev_plan[0], &ctx->ev_plan[1], &ctx->ev_step[0], &ctx->ev_step[1],
+                        &ctx->ev_tmp};
+  for (auto* e : evs)
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
+  if (cudaMemset(ctx->arena + lay.ticket, 0, 64) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
+  ctx->slot_base.assign(desc->L, 0);
+  ctx->ids_h.resize((size_t)desc->max_batch * desc->K);
+  ctx->w_h.resize((size_t)desc->max_batch * desc->K);
+  ctx->rank_h.resize(desc->N);
+  *out = ctx;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_load_router(moepic_ctx* ctx, int32_t layer, const uint16_t* w_bf16) {
+  CTX_GUARD();
+  if (layer < 0 || layer >= ctx->desc.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
+  if (!w_bf16) return fail(&ctx->err, MOEPIC_EINVAL, "w_bf16 is NULL");
+  CK(cudaMemcpy((void*)ctx->router(layer), w_bf16, (size_t)ctx->desc.N * ctx->desc.d * 2,
+                cudaMemcpyHostToDevice));
+  return MOEPIC_OK;
+}
+
+// HF layout -> row-interleaved rows [gate_r | up_r | down[:, r]]
+static void pack_rows(uint8_t* dst, const uint16_t* gate, const uint16_t* up, const uint16_t* down, int d,
+                      int I) {
+  const size_t rowe = 3ull * d;
+  uint16_t* o = reinterpret_cast<uint16_t*>(dst);
+#pragma omp parallel for schedule(static)
+  for (int rb = 0; rb < I; rb += 64) {
+    const int re = std::min(I, rb + 64);
+    for (int r = rb; r < re; ++r) {
+      memcpy(o + (size_t)r * rowe, gate + (size_t)r * d, (size_t)d * 2);
+      memcpy(o + (size_t)r * rowe + d, up + (size_t)r * d, (size_t)d * 2);
+    }
+    for (int k0 = 0; k0 < d; k0 += 64) {
+      const int ke = std::min(d, k0 + 64);
+      for (int r = rb; r < re; ++r) {
+        uint16_t* orow = o + (size_t)r * rowe + 2 * d;
+        for (int k = k0; k < ke; ++k) orow[k] = down[(size_t)k * I + r];
+      }
+    }
+  }
+}
+
+moepic_status moepic_load_expert(moepic_ctx* ctx, int32_t layer, int32_t expert, const uint16_t* gate,
+                                 const uint16_t* up, const uint16_t* down) {
+  CTX_GUARD();
+  const auto& d = ctx->desc;
+  if (!gate || !up || !down) return fail(&ctx->err, MOEPIC_EINVAL, "weight pointer is NULL");
+  if (expert >= 0) {
+    if (expert >= d.N) return fail(&ctx->err, MOEPIC_EINVAL, "expert out of range");
+    if (layer < 0 || layer >= d.L_host) return fail(&ctx->err, MOEPIC_EINVAL, "layer must be < L_host");
+    if (!ctx->cp->is_local(expert)) return MOEPIC_OK;   // another EP rank owns it
+    pack_rows(const_cast<uint8_t*>(ctx->host_expert(layer, expert)), gate, up, down, d.d, d.I);
+    return MOEPIC_OK;
+  }
+  const int s = -1 - expert;
+  if (s >= d.n_shared) return fail(&ctx->err, MOEPIC_EINVAL, "shared expert index out of range");
+  if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
+  std::vector<uint8_t> tmp((size_t)d.I * ctx->rb());
+  pack_rows(tmp.data(), gate, up, down, d.d, d.I);
+  CK(cudaMemcpy(ctx->shared_ptr(layer, s), tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg, moepic_config_out* out) {
+  CTX_GUARD();
+  if (!cfg) return fail(&ctx->err, MOEPIC_EINVAL, "cfg is NULL");
+  if (cfg->v_e > ctx->desc.v_e_max + 1e-9) return fail(&ctx->err, MOEPIC_EINVAL, "v_e exceeds v_e_max");
+  CK(cudaDeviceSynchronize());        // "when the device is idle"
+  std::string e = ctx->cp->configure(to_params(cfg, ctx->desc.L), ctx->lay.pool_rows);
+  if (!e.empty()) return fail(&ctx->err, MOEPIC_EINVAL, "%s", e.c_str());
+  // re-layout: per-layer slot regions, tops of cached experts H2D
+  uint64_t off = 0;
+  const uint64_t rb = ctx->rb();
+  for (int i = 0; i < ctx->desc.L; ++i) {
+    const LayerState& l = ctx->cp->layers[i];
+    ctx->slot_base[i] = off;
+    if (!l.cache_on()) continue;
+    off += (uint64_t)l.C * l.I_top * rb;
+  }
+  for (int i = 0; i < ctx->desc.L; ++i) {
+    const LayerState& l = ctx->cp->layers[i];
+    if (!l.cache_on()) continue;
+    for (int s = 0; s < (int)l.slot_expert.size(); ++s) {
+      const int ex = l.slot_expert[s];
+      if (ex < 0) continue;
+      CK(cudaMemcpyAsync(ctx->slot_ptr(i, s), ctx->host_expert(i, ex), (size_t)l.I_top * rb,
+                         cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies++;
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->copy));
+  ctx->pending = Plan();
+  ctx->configured = true;
+  write_config_out(*ctx->cp, out);
+  return MOEPIC_OK;
+}
+
+// Build K2 launches + combine segments for one group of segments.
+struct StepSeg {
+  const uint8_t* base;
+  int32_t expert, nrows;
+  uint32_t mask;
+};
+
+static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& segs, const uint16_t* h, int B,
+                                  cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb, int& launches) {
+  const int d = ctx->desc.d;
+  const int tbmax = k2_max_tokens(d);
+  // split by token groups of <= tbmax tokens
+  std::vector<StepSeg> work;
+  for (const auto& sg : segs) {
+    if (sg.nrows <= 0 || sg.mask == 0) continue;
+    uint32_t m = sg.mask;
+    while (m) {
+      uint32_t part = 0;
+      for (int t = 0; t < tbmax && m; ++t) {
+        uint32_t low = m & (~m + 1u);
+        part |= low;
+        m &= m - 1u;
+      }
+      StepSeg x = sg;
+      x.mask = part;
+      work.push_back(x);
+    }
+  }
+  size_t i0 = 0;
+  static K2Params kp;   // large; ctx calls are serialised by contract
+  while (i0 < work.size()) {
+    const size_t i1 = std::min(work.size(), i0 + (size_t)kMaxLaunchSegs);
+    int64_t R = 0;
+    int maxtok = 1;
+    for (size_t i = i0; i < i1; ++i) {
+      R += work[i].nrows;
+      maxtok = std::max(maxtok, __builtin_popcount(work[i].mask));
+    }
+    const int64_t G = std::min<int64_t>(kSMs, R);
+    kp.h = h;
+    kp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids);
+    kp.w = reinterpret_cast<const float*>(ctx->arena + ctx->lay.w);
+    kp.ws = reinterpret_cast<float*>(ctx->arena + ctx->lay.ws);
+    kp.total_rows = R;
+    kp.d = d;
+    kp.K = ctx->desc.K;
+    kp.nsegs = (int)(i1 - i0);
+    int64_t rb = 0;
+    for (size_t i = i0; i < i1; ++i) {
+      Seg& g = kp.segs[i - i0];
+      g.base = work[i].base;
+      g.expert = work[i].expert;
+      g.nrows = work[i].nrows;
+      g.tok_mask = work[i].mask;
+      g.row_begin = (int32_t)rb;
+      // CTA owning the first / last row: largest c with c*R/G <= row
+      const int64_t first = rb, last = rb + work[i].nrows - 1;
+      int64_t cf = (first * G) / R;
+      while (cf + 1 < G && k2_row_lo(cf + 1, R, G) <= first) ++cf;
+      while (k2_row_lo(cf, R, G) > first) --cf;
+      int64_t cl = (last * G) / R;
+      while (cl + 1 < G && k2_row_lo(cl + 1, R, G) <= last) ++cl;
+      while (k2_row_lo(cl, R, G) > last) --cl;
+      g.cta_first = (int32_t)cf;
+      const int ntok = __builtin_popcount(work[i].mask);
+      const int nchunks = (int)(cl - cf + 1);
+      g.ws_off = ws_next;
+      comb.push_back(CombineSeg{ws_next, nchunks, work[i].mask});
+      ws_next += (int64_t)nchunks * ntok * d;
+      rb += work[i].nrows;
+    }
+    if ((uint64_t)ws_next > ctx->lay.ws_floats)
+      return fail(&ctx->err, MOEPIC_ERUNTIME, "workspace overflow (%lld floats)", (long long)ws_next);
+    int tb = 1;
+    while (tb < maxtok) tb <<= 1;
+    uint64_t alg_bytes = (uint64_t)R * ctx->rb();
+    for (size_t i = i0; i < i1; ++i) alg_bytes += (uint64_t)__builtin_popcount(work[i].mask) * d * 2;
+    const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
+    launch_k2(kp, (int)G, tb, s);
+    ctx->prof_end(pe, s, alg_bytes);
+    CK(cudaGetLastError());
+    ++launches;
+    i0 = i1;
+  }
+  return MOEPIC_OK;
+}
+
+static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s) {
+  volatile uint32_t* seqp = reinterpret_cast<volatile uint32_t*>(ctx->mailbox);
+  auto t0 = std::chrono::steady_clock::now();
+  uint64_t spins = 0;
+  while (*seqp != ctx->seq) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+    if ((++spins & 0xFFF) == 0) {
+      cudaError_t q = cudaStreamQuery(s);
+      if (q != cudaSuccess && q != cudaErrorNotReady) {
+        ctx->poisoned = true;
+        return fail(&ctx->err, MOEPIC_ERUNTIME, "router kernel failed: %s", cudaGetErrorString(q));
+      }
+      if (q == cudaSuccess && *seqp != ctx->seq) {
+        ctx->poisoned = true;
+        return fail(&ctx->err, MOEPIC_ERUNTIME, "router mailbox not published");
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
+        ctx->poisoned = true;
+        return fail(&ctx->err, MOEPIC_ERUNTIME, "router mailbox timeout");
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return MOEPIC_OK;
+}
+
+static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int layer_route, int layer_pred,
+                                cudaStream_t s, bool read_ids, bool read_rank) {
+  const auto& d = ctx->desc;
+  RouterParams rp{};
+  rp.h = h;
+  rp.W0 = layer_route >= 0 ? ctx->router(layer_route) : nullptr;
+  rp.W1 = layer_pred >= 0 ? ctx->router(layer_pred) : nullptr;
+  rp.logits = reinterpret_cast<double*>(ctx->arena + ctx->lay.logits);
+  rp.ids = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.ids);
+  rp.w = reinterpret_cast<float*>(ctx->arena + ctx->lay.w);
+  rp.ranking = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.ranking);
+  rp.ticket = reinterpret_cast<unsigned int*>(ctx->arena + ctx->lay.ticket);
+  uint8_t* mb = ctx->mailbox_dev;
+  rp.mb_seq = reinterpret_cast<volatile uint32_t*>(mb);
+  rp.mb_ids = reinterpret_cast<int32_t*>(mb + 64);
+  rp.mb_w = reinterpret_cast<float*>(mb + 64 + (size_t)d.max_batch * d.K * 4);
+  rp.mb_rank = reinterpret_cast<int32_t*>(mb + 64 + (size_t)d.max_batch * d.K * 8);
+  rp.seq = ++ctx->seq;
+  rp.B = B; rp.d = d.d; rp.N = d.N; rp.K = d.K; rp.renorm = d.renorm_topk;
+  const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_ROUTER);
+  launch_router(rp, s);
+  ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
+  CK(cudaGetLastError());
+  ctx->ctr.kernel_launches++;
+  moepic_status st = wait_mailbox(ctx, s);
+  if (st != MOEPIC_OK) return st;
+  const uint8_t* hb = ctx->mailbox;
+  if (read_ids) {
+    memcpy(ctx->ids_h.data(), hb + 64, (size_t)B * d.K * 4);
+    memcpy(ctx->w_h.data(), hb + 64 + (size_t)d.max_batch * d.K * 4, (size_t)B * d.K * 4);
+  }
+  if (read_rank) memcpy(ctx->rank_h.data(), hb + 64 + (size_t)d.max_batch * d.K * 8, (size_t)d.N * 4);
+  return MOEPIC_OK;
+}
+
+// Issue the plan's H2D copies into ping-pong half `buf`.
+static moepic_status issue_plan(moepic_ctx* ctx, Plan& plan, int buf) {
+  plan.buf = buf;
+  if (ctx->ev_step_rec[buf]) CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[buf], 0));
+  const int j = plan.target;
+  const LayerState& l = ctx->cp->layers[j];
+  const uint64_t rb = ctx->rb();
+  for (const auto& it : plan.items) {
+    const uint8_t* src = ctx->host_expert(j, it.expert) + (it.full ? 0 : (uint64_t)l.I_top * rb);
+    CK(cudaMemcpyAsync(ctx->plan_ptr(buf, it.buf_row), src, (size_t)it.rows * rb, cudaMemcpyHostToDevice,
+                       ctx->copy));
+    ctx->ctr.h2d_copies++;
+  }
+  CK(cudaEventRecord(ctx->ev_plan[buf], ctx->copy));
+  const uint64_t pb = plan_bytes(plan, (int64_t)rb);
+  ctx->ctr.pcie_prefetch_bytes += pb;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B, float* y_dev,
+                                   void* stream, uint32_t flags, moepic_trace* tr) {
+  CTX_GUARD();
+  const auto& d = ctx->desc;
+  if (!ctx->configured) return fail(&ctx->err, MOEPIC_EINVAL, "moepic_configure has not been called");
+  if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
+  if (B < 1 || B > d.max_batch) return fail(&ctx->err, MOEPIC_EINVAL, "B must be in [1, max_batch]");
+  if (!h_dev || !y_dev) return fail(&ctx->err, MOEPIC_EINVAL, "h_dev / y_dev is NULL");
+  if ((reinterpret_cast<uintptr_t>(h_dev) & 15) || (reinterpret_cast<uintptr_t>(y_dev) & 15))
+    return fail(&ctx->err, MOEPIC_EINVAL, "h_dev and y_dev must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint16_t* h = static_cast<const uint16_t*>(h_dev);
+  const bool predict = (flags & MOEPIC_FUSE_PREDICT) != 0;
+  const int j = (layer + 1) % d.L;
+  ControlPlane& cp = *ctx->cp;
+  const LayerState& l = cp.layers[layer];
+  const uint64_t rb = ctx->rb();
+  int launches = 0;
+
+  Plan used;
+  const bool have_plan = ctx->pending.valid && ctx->pending.target == layer;
+  if (have_plan) used = std::move(ctx->pending);
+  ctx->pending = Plan();
+  const int buf = have_plan ? used.buf : (ctx->last_buf ^ 1);
+
+  // ---- K1 (router + fused next-layer predictor) and the mailbox handoff
+  moepic_status st = run_router(ctx, h, B, layer, predict ? j : -1, s, true, predict);
+  if (st != MOEPIC_OK) return st;
+  ++launches;
+
+  // ---- control plane (classification, counters, admission)
+  StepResult res;
+  cp.step(layer, ctx->ids_h.data(), B, have_plan ? &used : nullptr, res);
+
+  // token masks per activated expert
+  const int K = d.K;
+  auto mask_of = [&](int e) {
+    uint32_t m = 0;
+    for (int b = 0; b < B; ++b)
+      for (int k = 0; k < K; ++k)
+        if (ctx->ids_h[b * K + k] == e) m |= 1u << b;
+    return m;
+  };
+  std::vector<int32_t> adm_slot(d.N, -2);   // expert -> slot for admitted, -1 if not admitted
+  for (const auto& a : res.adm) adm_slot[a.expert] = a.victim == kAdmNone ? -1 : a.slot;
+
+  // ---- on-demand copies (transfer engine, copy stream, FIFO after the pending prefetch)
+  for (int b2 = 0; b2 < 2; ++b2)
+    if (ctx->ev_step_rec[b2]) CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[b2], 0));
+  std::vector<StepSeg> gA, gB, gC;
+  int64_t od_row = 0;
+  bool any_od = false;
+  const uint32_t all_tok = B >= 32 ? 0xFFFFFFFFu : ((1u << B) - 1u);
+  for (int s2 = 0; s2 < d.n_shared; ++s2) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2), -1 - s2, d.I, all_tok});
+  for (size_t a = 0; a < res.A.size(); ++a) {
+    const int e = res.A[a];
+    const uint32_t m = mask_of(e);
+    const int c = res.cls[a];
+    const int pj = res.plan_idx[a];
+    const uint8_t* hsrc = ctx->host_expert(layer, e);
+    const bool top_cached_before = (c != kGamma) && !(pj >= 0 && used.items[pj].full);
+    if (top_cached_before && l.I_top > 0) {
+      gA.push_back(StepSeg{ctx->slot_ptr(layer, l.slot_of[e]), e, l.I_top, m});
+    }
+    if (pj >= 0) {
+      const PlanItem& it = used.items[pj];
+      gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m});
+      continue;   // alpha: nothing missing
+    }
+    if (c == kBeta) {
+      const int rows = d.I - l.I_top;
+      uint8_t* dst = ctx->od_ptr(buf, od_row);
+      CK(cudaMemcpyAsync(dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows * rb, cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies++;
+      gC.push_back(StepSeg{dst, e, rows, m});
+      od_row += rows;
+      any_od = true;
+    } else if (c == kGamma) {
+      const int slot = adm_slot[e];
+      if (slot >= 0 && l.I_top > 0) {
+        uint8_t* top = ctx->slot_ptr(layer, slot);
+        CK(cudaMemcpyAsync(top, hsrc, (size_t)l.I_top * rb, cudaMemcpyHostToDevice, ctx->copy));
+        ctx->ctr.h2d_copies++;
+        gC.push_back(StepSeg{top, e, l.I_top, m});
+        const int rows = d.I - l.I_top;
+        if (rows > 0) {
+          uint8_t* dst = ctx->od_ptr(buf, od_row);
+          CK(cudaMemcpyAsync(dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows * rb, cudaMemcpyHostToDevice,
+                             ctx->copy));
+          ctx->ctr.h2d_copies++;
+          gC.push_back(StepSeg{dst, e, rows, m});
+          od_row += rows;
+        }
+      } else {
+        uint8_t* dst = ctx->od_ptr(buf, od_row);
+        CK(cudaMemcpyAsync(dst, hsrc, (size_t)d.I * rb, cudaMemcpyHostToDevice, ctx->copy));
+        ctx->ctr.h2d_copies++;
+        gC.push_back(StepSeg{dst, e, d.I, m});
+        od_row += d.I;
+      }
+      any_od = true;
+    }
+  }
+  if ((uint64_t)od_row > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+  if (any_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
+
+  // ---- K2 launches: resident now / prefetched / on-demand, then the combine
+  int64_t ws_next = 0;
+  std::vector<CombineSeg> comb;
+  st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches);
+  if (st != MOEPIC_OK) return st;
+  if (!gB.empty()) {
+    CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
+    st = launch_group(ctx, gB, h, B, s, ws_next, comb, launches);
+    if (st != MOEPIC_OK) return st;
+  }
+  if (!gC.empty()) {
+    CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
+    st = launch_group(ctx, gC, h, B, s, ws_next, comb, launches);
+    if (st != MOEPIC_OK) return st;
+  }
+  if (comb.size() > (size_t)kMaxStepSegs) return fail(&ctx->err, MOEPIC_ERUNTIME, "too many segments in one step");
+  static CombineParams cpar;
+  cpar.y = y_dev;
+  cpar.h = h;
+  cpar.ws = reinterpret_cast<const float*>(ctx->arena + ctx->lay.ws);
+  cpar.B = B;
+  cpar.d = d.d;
+  cpar.residual = (flags & MOEPIC_RESIDUAL) ? 1 : 0;
+  cpar.nsegs = (int)comb.size();
+  for (size_t i = 0; i < comb.size(); ++i) cpar.segs[i] = comb[i];
+  const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_COMBINE);
+  launch_combine(cpar, s);
+  {
+    uint64_t cb = (uint64_t)B * d.d * 4;
+    for (const auto& c : comb) cb += (uint64_t)c.nchunks * __builtin_popcount(c.tok_mask) * d.d * 4;
+    ctx->prof_end(pe, s, cb);
+  }
+  CK(cudaGetLastError());
+  ++launches;
+  // alpha experts that arrived as full prefetches and were admitted: D2D their top rows
+  for (const auto& a : res.adm) {
+    if (!a.d2d_from_plan || a.victim == kAdmNone || l.I_top == 0) continue;
+    const int pj = [&] { for (size_t k = 0; k < used.items.size(); ++k) if (used.items[k].expert == a.expert) return (int)k; return -1; }();
+    if (pj < 0) continue;
+    CK(cudaMemcpyAsync(ctx->slot_ptr(layer, a.slot), ctx->plan_ptr(buf, used.items[pj].buf_row),
+                       (size_t)l.I_top * rb, cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaEventRecord(ctx->ev_step[buf], s));
+  ctx->ev_step_rec[buf] = true;
+  ctx->last_buf = buf;
+
+  // ---- next-layer prefetch, issued after this layer's on-demand copies
+  Plan next;
+  if (predict) {
+    cp.make_plan(j, ctx->rank_h.data(), next);
+    st = issue_plan(ctx, next, buf ^ 1);
+    if (st != MOEPIC_OK) return st;
+    ctx->pending = next;
+  }
+
+  // ---- trace + counters
+  const uint64_t pb = predict ? plan_bytes(next, (int64_t)rb) : 0;
+  const uint64_t hbm = step_hbm_bytes(cp, res, B, predict ? 2 : 1, pb);
+  if (tr) {
+    for (int i = 0; i < B * K; ++i) {
+      if (tr->ids) tr->ids[i] = ctx->ids_h[i];
+      if (tr->w) tr->w[i] = ctx->w_h[i];
+    }
+    fill_step_trace(tr, res, predict ? &next : nullptr);
+    tr->pcie_prefetch_bytes = pb;
+    tr->hbm_bytes = hbm;
+    tr->kernel_launches = launches;
+  }
+  ctx->ctr.layer_steps++;
+  ctx->ctr.kernel_launches += launches - 1;   // router already counted
+  ctx->ctr.pcie_ondemand_bytes += res.pcie_ondemand;
+  ctx->ctr.hbm_bytes += hbm;
+  ctx->ctr.act_alpha += res.alpha;
+  ctx->ctr.act_beta += res.beta;
+  ctx->ctr.act_gamma += res.gamma;
+  ctx->ctr.pred_hits += res.pred_hits;
+  ctx->ctr.pred_total += res.A.size();
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const uint16_t* h_host, int32_t B,
+                                        float* y_host, void* stream, uint32_t flags, moepic_trace* tr) {
+  CTX_GUARD();
+  const auto& d = ctx->desc;
+  if (!h_host || !y_host) return fail(&ctx->err, MOEPIC_EINVAL, "h_host / y_host is NULL");
+  if (B < 1 || B > d.max_batch) return fail(&ctx->err, MOEPIC_EINVAL, "B must be in [1, max_batch]");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t hb = (size_t)B * d.d * 2, yb = (size_t)B * d.d * 4;
+  const size_t hoff = 0, yoff = align_up(hb);
+  const size_t need = yoff + yb;
+  if (ctx->scratch_bytes < need) {
+    if (ctx->scratch_h) cudaFreeHost(ctx->scratch_h);
+    ctx->scratch_h = nullptr;
+    ctx->scratch_bytes = 0;
+    CK(cudaHostAlloc(&ctx->scratch_h, need, cudaHostAllocDefault));
+    ctx->scratch_bytes = need;
+  }
+  if (ctx->dev_stage_bytes < need) {
+    if (ctx->dev_stage) cudaFree(ctx->dev_stage);
+    ctx->dev_stage = nullptr;
+    ctx->dev_stage_bytes = 0;
+    CK(cudaMalloc(&ctx->dev_stage, need));
+    ctx->dev_stage_bytes = need;
+  }
+  memcpy(ctx->scratch_h + hoff, h_host, hb);
+  uint8_t* ds = static_cast<uint8_t*>(ctx->dev_stage);
+  CK(cudaMemcpyAsync(ds + hoff, ctx->scratch_h + hoff, hb, cudaMemcpyHostToDevice, s));
+  moepic_status st = moepic_layer_forward(ctx, layer, ds + hoff, B, reinterpret_cast<float*>(ds + yoff), stream,
+                                          flags, tr);
+  if (st != MOEPIC_OK) return st;
+  CK(cudaMemcpyAsync(ctx->scratch_h + yoff, ds + yoff, yb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  memcpy(y_host, ctx->scratch_h + yoff, yb);
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_predict_prefetch(moepic_ctx* ctx, int32_t next_layer, const void* h_dev, int32_t B,
+                                      void* stream, moepic_trace* tr) {
+  CTX_GUARD();
+  const auto& d = ctx->desc;
+  if (!ctx->configured) return fail(&ctx->err, MOEPIC_EINVAL, "moepic_configure has not been called");
+  if (next_layer < 0 || next_layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "next_layer out of range");
+  if (B < 1 || B > d.max_batch) return fail(&ctx->err, MOEPIC_EINVAL, "B must be in [1, max_batch]");
+  if (!h_dev || (reinterpret_cast<uintptr_t>(h_dev) & 15))
+    return fail(&ctx->err, MOEPIC_EINVAL, "h_dev must be a 16-byte aligned device pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  moepic_status st = run_router(ctx, static_cast<const uint16_t*>(h_dev), B, -1, next_layer, s, false, true);
+  if (st != MOEPIC_OK) return st;
+  Plan next;
+  ctx->cp->make_plan(next_layer, ctx->rank_h.data(), next);
+  ctx->pending = Plan();
+  st = issue_plan(ctx, next, ctx->last_buf ^ 1);
+  if (st != MOEPIC_OK) return st;
+  ctx->pending = next;
+  if (tr) {
+    StepResult empty;
+    fill_step_trace(tr, empty, &next);
+    tr->n_act = 0;
+    tr->n_adm = 0;
+    tr->pcie_ondemand_bytes = 0;
+    tr->pcie_prefetch_bytes = plan_bytes(next, (int64_t)ctx->rb());
+    tr->hbm_bytes = tr->pcie_prefetch_bytes + (uint64_t)d.N * d.d * 2;
+    tr->kernel_launches = 1;
+  }
+  return MOEPIC_OK;
+}
+
+// statistics snapshot: header {L, N, K} then per layer: q, q_pred, freq[N], rank_hit[N+1],
+// pred_hit[N+1], pred_rank[(N+1)^2], mu[N], nu[N], last[N], step_no   (all int64)
+static size_t stats_bytes(const moepic_model_desc& d) {
+  const size_t N = d.N;
+  return 8 * (3 + (size_t)d.L * (2 + N + (N + 1) + (N + 1) + (N + 1) * (N + 1) + 3 * N + 1));
+}
+
+moepic_status moepic_get_stats(moepic_ctx* ctx, void* buf, size_t* bytes) {
+  CTX_GUARD();
+  if (!bytes) return fail(&ctx->err, MOEPIC_EINVAL, "bytes is NULL");
+  const size_t need = stats_bytes(ctx->desc);
+  if (!buf) { *bytes = need; return MOEPIC_OK; }
+  if (*bytes < need) return fail(&ctx->err, MOEPIC_EINVAL, "buffer too small (%zu < %zu)", *bytes, need);
+  int64_t* o = static_cast<int64_t*>(buf);
+  *o++ = ctx->desc.L; *o++ = ctx->desc.N; *o++ = ctx->desc.K;
+  for (const auto& l : ctx->cp->layers) {
+    *o++ = l.st.q; *o++ = l.st.q_pred;
+    for (auto v : l.st.freq) *o++ = v;
+    for (auto v : l.st.rank_hit) *o++ = v;
+    for (auto v : l.st.pred_hit) *o++ = v;
+    for (auto v : l.st.pred_rank) *o++ = v;
+    for (auto v : l.mu) *o++ = v;
+    for (auto v : l.nu) *o++ = v;
+    for (auto v : l.last) *o++ = v;
+    *o++ = l.step_no;
+  }
+  *bytes = need;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_set_stats(moepic_ctx* ctx, const void* buf, size_t bytes) {
+  CTX_GUARD();
+  if (!buf || bytes != stats_bytes(ctx->desc)) return fail(&ctx->err, MOEPIC_EINVAL, "snapshot size mismatch");
+  const int64_t* in = static_cast<const int64_t*>(buf);
+  if (in[0] != ctx->desc.L || in[1] != ctx->desc.N || in[2] != ctx->desc.K)
+    return fail(&ctx->err, MOEPIC_EINVAL, "snapshot shape (L, N, K) mismatch");
+  in += 3;
+  for (auto& l : ctx->cp->layers) {
+    l.st.q = *in++; l.st.q_pred = *in++;
+    for (auto& v : l.st.freq) v = *in++;
+    for (auto& v : l.st.rank_hit) v = *in++;
+    for (auto& v : l.st.pred_hit) v = *in++;
+    for (auto& v : l.st.pred_rank) v = *in++;
+    for (auto& v : l.mu) v = *in++;
+    for (auto& v : l.nu) v = *in++;
+    for (auto& v : l.last) v = *in++;
+    l.step_no = *in++;
+    l.st.dirty = true;
+  }
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_get_counters(moepic_ctx* ctx, moepic_counters* out) {
+  CTX_GUARD();
+  if (!out) return MOEPIC_EINVAL;
+  *out = ctx->ctr;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable) {
+  CTX_GUARD();
+  ctx->prof_drain();
+  for (auto& k : ctx->prof_acc) k = moepic_kernel_stats{};
+  ctx->profiling = enable != 0;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_kernel_stats* out) {
+  CTX_GUARD();
+  if (!out || kernel_class < 0 || kernel_class > 2) return fail(&ctx->err, MOEPIC_EINVAL, "bad profile_read args");
+  ctx->prof_drain();
+  *out = ctx->prof_acc[kernel_class];
+  return MOEPIC_OK;
+}
+
+const char* moepic_last_error(const moepic_ctx* ctx) { return ctx ? ctx->err.c_str() : "ctx is NULL"; }
+
+void moepic_destroy(moepic_ctx* ctx) {
+  if (!ctx) return;
+  cudaDeviceSynchronize();
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  for (auto& pe : ctx->prof) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
+  cudaEvent_t evs[] = {ctx->ev_od, ctx->ev_plan[0], ctx->ev_plan[1], ctx->ev_step[0], ctx->ev_step[1], ctx->ev_tmp};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  if (ctx->host_experts) cudaFreeHost(ctx->host_experts);
+  if (ctx->mailbox) cudaFreeHost(ctx->mailbox);
+  if (ctx->scratch_h) cudaFreeHost(ctx->scratch_h);
+  if (ctx->dev_stage) cudaFree(ctx->dev_stage);
+  delete ctx;
+}
+
+// ====================================================================== host-only simulator
+struct moepic_hostsim {
+  moepic_model_desc desc{};
+  std::unique_ptr<ControlPlane> cp;
+  ArenaLayout lay{};
+  Plan pending;
+  std::string err;
+};
+
+moepic_status moepic_hostsim_create(const moepic_model_desc* desc, moepic_hostsim** out) {
+  if (!out) return MOEPIC_EINVAL;
+  *out = nullptr;
+  if (!validate_desc(desc).empty()) return MOEPIC_EINVAL;
+  auto* hs = new (std::nothrow) moepic_hostsim();
+  if (!hs) return MOEPIC_ENOMEM;
+  hs->desc = *desc;
+  hs->lay = arena_layout(*desc);
+  hs->cp.reset(new ControlPlane(desc->L, desc->N, desc->K, desc->d, desc->I, desc->row_granule,
+                                desc->buffer_experts, desc->n_shared, desc->ep_rank, desc->ep_size));
+  *out = hs;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_hostsim_configure(moepic_hostsim* hs, const moepic_cache_config* cfg,
+                                       moepic_config_out* out) {
+  if (!hs) return MOEPIC_EINVAL;
+  if (!cfg) return fail(&hs->err, MOEPIC_EINVAL, "cfg is NULL");
+  if (cfg->v_e > hs->desc.v_e_max + 1e-9) return fail(&hs->err, MOEPIC_EINVAL, "v_e exceeds v_e_max");
+  std::string e = hs->cp->configure(to_params(cfg, hs->desc.L), hs->lay.pool_rows);
+  if (!e.empty()) return fail(&hs->err, MOEPIC_EINVAL, "%s", e.c_str());
+  hs->pending = Plan();
+  write_config_out(*hs->cp, out);
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_hostsim_step(moepic_hostsim* hs, int32_t layer, const int32_t* ids, int32_t B,
+                                  int32_t next_layer, const int32_t* ranking_next, moepic_trace* tr) {
+  if (!hs) return MOEPIC_EINVAL;
+  const auto& d = hs->desc;
+  if (!hs->cp->configured) return fail(&hs->err, MOEPIC_EINVAL, "not configured");
+  if (layer < 0 || layer >= d.L) return fail(&hs->err, MOEPIC_EINVAL, "layer out of range");
+  if (B < 1 || B > 4096 || !ids) return fail(&hs->err, MOEPIC_EINVAL, "bad ids / B");
+  for (int i = 0; i < B * d.K; ++i)
+    if (ids[i] < 0 || ids[i] >= d.N) return fail(&hs->err, MOEPIC_EINVAL, "expert id out of range");
+  if (ranking_next && (next_layer < 0 || next_layer >= d.L)) return fail(&hs->err, MOEPIC_EINVAL, "next_layer out of range");
+  Plan used;
+  const bool have = hs->pending.valid && hs->pending.target == layer;
+  if (have) used = std::move(hs->pending);
+  hs->pending = Plan();
+  StepResult res;
+  hs->cp->step(layer, ids, B, have ? &used : nullptr, res);
+  Plan next;
+  if (ranking_next) {
+    hs->cp->make_plan(next_layer, ranking_next, next);
+    hs->pending = next;
+  }
+  const uint64_t pb = ranking_next ? plan_bytes(next, hs->cp->row_bytes) : 0;
+  if (tr) {
+    fill_step_trace(tr, res, ranking_next ? &next : nullptr);
+    tr->pcie_prefetch_bytes = pb;
+    tr->hbm_bytes = step_hbm_bytes(*hs->cp, res, B, ranking_next ? 2 : 1, pb);
+    tr->kernel_launches = 0;
+  }
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_hostsim_predict(moepic_hostsim* hs, int32_t next_layer, const int32_t* ranking,
+                                     moepic_trace* tr) {
+  if (!hs) return MOEPIC_EINVAL;
+  if (!hs->cp->configured) return fail(&hs->err, MOEPIC_EINVAL, "not configured");
+  if (next_layer < 0 || next_layer >= hs->desc.L || !ranking) return fail(&hs->err, MOEPIC_EINVAL, "bad args");
+  Plan next;
+  hs->cp->make_plan(next_layer, ranking, next);
+  hs->pending = next;
+  if (tr) {
+    StepResult empty;
+    fill_step_trace(tr, empty, &next);
+    tr->pcie_prefetch_bytes = plan_bytes(next, hs->cp->row_bytes);
+    tr->hbm_bytes = tr->pcie_prefetch_bytes + (uint64_t)hs->desc.N * hs->desc.d * 2;
+    tr->kernel_launches = 0;
+  }
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_hostsim_cached(moepic_hostsim* hs, int32_t layer, int32_t* out, int32_t* n) {
+  if (!hs || !out || !n || layer < 0 || layer >= hs->desc.L) return MOEPIC_EINVAL;
+  int c = 0;
+  const LayerState& l = hs->cp->layers[layer];
+  for (int e = 0; e < hs->desc.N; ++e)
+    if (l.cached(e)) out[c++] = e;
+  *n = c;
+  return MOEPIC_OK;
+}
+
+const char* moepic_hostsim_last_error(const moepic_hostsim* hs) { return hs ? hs->err.c_str() : "hs is NULL"; }
+void moepic_hostsim_destroy(moepic_hostsim* hs) { delete hs; }
+
+}  // extern "C"
