@@ -51,7 +51,7 @@ class CacheConfig:
     t_att: float = 0.0
     t_moe: float = 0.0
     t_head: float = 0.0
-    t_load: float = 0.0
+    t_load_exp: float = 0.0
     y_cap_i: list | None = None
     prefetch: bool = True
     seed: int = 0
@@ -115,7 +115,7 @@ class OracleEngine:
             V0 = self.V if self.V is not None else (
                 list(cfg.v_i) if cfg.v_i is not None else [cfg.v_e / L] * L)
             V, th, C, _, _ = vram_allocation(self.stats, V0, cfg.v_e, cfg.zeta, K, N, float(self.U_b),
-                                             cfg.t_att, cfg.t_moe, cfg.t_head, cfg.t_load)
+                                             cfg.t_att, cfg.t_moe, cfg.t_head, cfg.t_load_exp)
             thetas = th
             Cs = C
         else:
