@@ -137,6 +137,33 @@ def moe_layer(h_bits, router_bits, experts, K, shared=(), renorm=True):
     return y, ids, w, logits
 
 
+def moe_layer_ep_partial(h_bits, router_bits, experts, K, ep_rank, ep_size, shared=(), renorm=True):
+    """Rank ep_rank's share of the layer output under expert parallelism:
+    the routed experts it owns (e * ep_size // N == ep_rank) plus rows
+    [r I / G, (r+1) I / G) of every shared expert (split identity).  Summing the shares
+    of all ranks gives moe_layer(...)[0]."""
+    h = bf16_to_f64(h_bits)
+    logits = router_logits(h_bits, router_bits)
+    B, d = h.shape
+    N = logits.shape[1]
+    get = experts if callable(experts) else (lambda e: experts[e])
+    y = np.zeros((B, d), dtype=np.float64)
+    for b in range(B):
+        ids = topk_ids(logits[b], K)
+        w = gate_weights(logits[b], ids, renorm)
+        for k, e in enumerate(ids):
+            if e * ep_size // N != ep_rank:
+                continue
+            gate, up, down = (bf16_to_f64(x) for x in get(int(e)))
+            y[b] += w[k] * expert_forward(h[b:b + 1], gate, up, down)[0]
+    for (gate, up, down) in shared:
+        g, u, dn = bf16_to_f64(gate), bf16_to_f64(up), bf16_to_f64(down)
+        I = g.shape[0]
+        lo, hi = ep_rank * I // ep_size, (ep_rank + 1) * I // ep_size
+        y += expert_forward(h, g[lo:hi], u[lo:hi], dn[:, lo:hi])
+    return y
+
+
 def predicted_ranking(pred_logits: np.ndarray, K: int) -> np.ndarray:
     """Next-layer ranking R' of all N experts (Eq. 3; reading Q9).
 

@@ -75,8 +75,13 @@ class StepTrace:
 
 
 class OracleEngine:
-    def __init__(self, L, N, K, d, I, row_granule=64, buffer_experts=None, n_shared=0, I_shared=None):
+    def __init__(self, L, N, K, d, I, row_granule=64, buffer_experts=None, n_shared=0, I_shared=None,
+                 ep_rank=0, ep_size=1):
         self.L, self.N, self.K, self.d, self.I = L, N, K, d, I
+        # expert parallelism: this engine is rank ep_rank of ep_size; it owns
+        # experts e with e * ep_size // N == ep_rank and the shared-expert rows
+        # [ep_rank * I // ep_size, (ep_rank + 1) * I // ep_size)
+        self.ep_rank, self.ep_size = ep_rank, ep_size
         self.g = row_granule
         self.U_b = K if buffer_experts is None else buffer_experts
         self.n_shared = n_shared
@@ -96,6 +101,12 @@ class OracleEngine:
         self.pending = None
 
     # ------------------------------------------------------------------ configure
+    def is_local(self, e) -> bool:
+        return e * self.ep_size // self.N == self.ep_rank
+
+    def shared_rows(self) -> int:
+        return (self.ep_rank + 1) * self.I_shared // self.ep_size - self.ep_rank * self.I_shared // self.ep_size
+
     def cache_on(self, i) -> bool:
         return self.C[i] > 0 and self.I_top[i] > 0
 
@@ -153,15 +164,16 @@ class OracleEngine:
             return []
         if self.stats[i].q == 0:
             if cfg.seed == 0:
-                return list(range(C))
-            perm, _ = P.fisher_yates(N, P.layer_stream_seed(cfg.seed, i, 2))
-            return perm[:C]
-        if cfg.policy == P.RND:
-            perm, self.rnd[i] = P.fisher_yates(N, self.rnd[i])
-            return perm[:C]
-        keyf = lambda e: P.policy_key(cfg.policy, self.mu[i][e], self.nu[i][e], self.last[i][e], cfg.rho, cfg.omega)
-        order = sorted(range(N), key=lambda e: (-keyf(e), self.nu[i][e], e))
-        return order[:C]
+                order = list(range(N))
+            else:
+                order, _ = P.fisher_yates(N, P.layer_stream_seed(cfg.seed, i, 2))
+        elif cfg.policy == P.RND:
+            order, self.rnd[i] = P.fisher_yates(N, self.rnd[i])
+        else:
+            keyf = lambda e: P.policy_key(cfg.policy, self.mu[i][e], self.nu[i][e], self.last[i][e], cfg.rho,
+                                          cfg.omega)
+            order = sorted(range(N), key=lambda e: (-keyf(e), self.nu[i][e], e))
+        return [e for e in order if self.is_local(e)][:C]
 
     # ------------------------------------------------------------------ planning
     def _plan(self, j, ranking):
@@ -175,6 +187,8 @@ class OracleEngine:
             e = int(e)
             if len(items) >= ycap:
                 break
+            if not self.is_local(e):
+                continue
             if self.cache_on(j) and e in self.cache[j]:
                 rows = self.I - self.I_top[j]
                 if rows == 0:
@@ -210,7 +224,7 @@ class OracleEngine:
         for b in range(B):
             for e in ids[b]:
                 Be[int(e)] = Be.get(int(e), 0) + 1
-        A = sorted(Be, key=lambda e: (-Be[e], e))
+        A = sorted((e for e in Be if self.is_local(e)), key=lambda e: (-Be[e], e))
         Aset = set(A)
         # 2. stats (pre-increment ranks)
         self.stats[i].observe(ids, plan.ranking if plan is not None else None)
@@ -281,6 +295,6 @@ class OracleEngine:
             tr.pcie_prefetch = sum(r for (_, _, r) in self.pending.items) * rb
         else:
             self.pending = None      # a step always consumes (or discards) the pending plan
-        tr.hbm = (len(A) * I * rb + self.n_shared * self.I_shared * rb + n_router * N * self.d * 2
+        tr.hbm = (len(A) * I * rb + self.n_shared * self.shared_rows() * rb + n_router * N * self.d * 2
                   + B * self.d * 2 + B * self.d * 4 + d2d + tr.pcie_ondemand + tr.pcie_prefetch)
         return tr

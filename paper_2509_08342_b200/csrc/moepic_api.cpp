@@ -121,10 +121,14 @@ void write_config_out(const ControlPlane& cp, moepic_config_out* out) {
   }
 }
 
+// shared-expert rows this EP rank computes: [r*I/G, (r+1)*I/G) (split identity)
+inline int64_t shared_lo(const ControlPlane& cp) { return (int64_t)cp.ep_rank * cp.I / cp.ep_size; }
+inline int64_t shared_hi(const ControlPlane& cp) { return (int64_t)(cp.ep_rank + 1) * cp.I / cp.ep_size; }
+
 uint64_t step_hbm_bytes(const ControlPlane& cp, const StepResult& r, int B, int n_router,
                         uint64_t prefetch_bytes) {
   const uint64_t rb = (uint64_t)cp.row_bytes;
-  return (uint64_t)r.A.size() * cp.I * rb + (uint64_t)cp.n_shared * cp.I * rb +
+  return (uint64_t)r.A.size() * cp.I * rb + (uint64_t)cp.n_shared * (shared_hi(cp) - shared_lo(cp)) * rb +
          (uint64_t)n_router * cp.N * cp.d * 2 + (uint64_t)B * cp.d * 2 + (uint64_t)B * cp.d * 4 + r.d2d_bytes +
          r.pcie_ondemand + prefetch_bytes;
 }
@@ -634,7 +638,11 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   int64_t od_row = 0;
   bool any_od = false;
   const uint32_t all_tok = B >= 32 ? 0xFFFFFFFFu : ((1u << B) - 1u);
-  for (int s2 = 0; s2 < d.n_shared; ++s2) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2), -1 - s2, d.I, all_tok});
+  {
+    const int64_t lo = shared_lo(cp), hi = shared_hi(cp);
+    for (int s2 = 0; s2 < d.n_shared; ++s2)
+      if (hi > lo) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2) + lo * rb, -1 - s2, (int32_t)(hi - lo), all_tok});
+  }
   for (size_t a = 0; a < res.A.size(); ++a) {
     const int e = res.A[a];
     const uint32_t m = mask_of(e);
@@ -709,7 +717,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   cpar.ws = reinterpret_cast<const float*>(ctx->arena + ctx->lay.ws);
   cpar.B = B;
   cpar.d = d.d;
-  cpar.residual = (flags & MOEPIC_RESIDUAL) ? 1 : 0;
+  cpar.residual = ((flags & MOEPIC_RESIDUAL) && d.ep_rank == 0) ? 1 : 0;   // h added once across ranks
   cpar.nsegs = (int)comb.size();
   for (size_t i = 0; i < comb.size(); ++i) cpar.segs[i] = comb[i];
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_COMBINE);
