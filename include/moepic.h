@@ -98,6 +98,11 @@ typedef struct {
   const int32_t* y_cap_i;  /* [L] max prefetch count per layer, or NULL (buffer-bound)          */
   int32_t prefetch;        /* 0: no speculative prefetch (cache-only baseline); 1: on          */
   uint64_t seed;           /* splitmix64 seed: initial random cached set, RND victims   */
+  int32_t cancel_prefetch; /* 1: prefetch is fed in chunks while the host waits for routing and
+                              the unissued chunks of experts the router did not activate are
+                              dropped ("terminates the prefetch operation").  Plans,
+                              classes and traces are unchanged; only the bytes actually moved
+                              (moepic_counters) differ.  0: every planned byte is transferred.  */
 } moepic_cache_config;
 
 /* configure output: caller-owned arrays of length L (any may be NULL) */
@@ -193,6 +198,8 @@ typedef struct {
   uint64_t pcie_ondemand_bytes, pcie_prefetch_bytes, hbm_bytes;
   uint64_t act_alpha, act_beta, act_gamma;    /* class counts over all steps                  */
   uint64_t pred_hits, pred_total;             /* activated experts that were planned / total  */
+  uint64_t pcie_prefetch_planned_bytes;       /* planned prefetch bytes (pcie_prefetch_bytes
+                                                 counts what was actually transferred)        */
 } moepic_counters;
 moepic_status moepic_get_counters(moepic_ctx* ctx, moepic_counters* out);
 

@@ -42,7 +42,7 @@ class moepic_cache_config(C.Structure):
                 ("policy", C.c_int32), ("rho", C.c_double), ("omega", C.c_int32), ("zeta", C.c_double),
                 ("t_att", C.c_double), ("t_moe", C.c_double), ("t_head", C.c_double),
                 ("t_load_exp", C.c_double), ("y_cap_i", _i32p), ("prefetch", C.c_int32),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("cancel_prefetch", C.c_int32)]
 
 
 class moepic_config_out(C.Structure):
@@ -62,7 +62,8 @@ class moepic_trace(C.Structure):
 class moepic_counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "layer_steps", "kernel_launches", "h2d_copies", "pcie_ondemand_bytes", "pcie_prefetch_bytes",
-        "hbm_bytes", "act_alpha", "act_beta", "act_gamma", "pred_hits", "pred_total")]
+        "hbm_bytes", "act_alpha", "act_beta", "act_gamma", "pred_hits", "pred_total",
+        "pcie_prefetch_planned_bytes")]
 
 
 class moepic_kernel_stats(C.Structure):

@@ -196,6 +196,51 @@ struct moepic_ctx {
     int cls;
     uint64_t bytes;
   };
+  // prefetch feed queue (cancel_prefetch): chunks of the pending plan, issued a few at a
+  // time on the copy stream while the host waits for routing; unissued chunks of experts that
+  // the router did not activate are dropped
+  struct FeedChunk {
+    uint8_t* dst;
+    const uint8_t* src;
+    size_t bytes;
+    int32_t item;
+  };
+  static constexpr size_t kFeedChunk = 8ull << 20;
+  static constexpr size_t kFeedDepth = 3;
+  static constexpr int kFeedRing = 16;
+  bool cancel_prefetch = true;
+  std::vector<FeedChunk> feed;
+  size_t feed_next = 0;
+  std::vector<char> feed_cancel;
+  cudaEvent_t feed_ev[kFeedRing] = {};
+  int feed_ev_next = 0;
+  std::vector<int> feed_inflight;   // ring indices, oldest first
+
+  // issue chunks until `depth` are in flight; returns false on a CUDA error
+  bool feed_pump(size_t depth) {
+    while (!feed_inflight.empty() && cudaEventQuery(feed_ev[feed_inflight.front()]) == cudaSuccess)
+      feed_inflight.erase(feed_inflight.begin());
+    const bool track = depth != (size_t)-1;
+    while (feed_next < feed.size() && feed_inflight.size() < depth) {
+      const FeedChunk& c = feed[feed_next++];
+      if (feed_cancel[c.item]) continue;
+      if (cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, copy) != cudaSuccess) return false;
+      ctr.h2d_copies++;
+      ctr.pcie_prefetch_bytes += c.bytes;
+      if (!track) continue;
+      const int e = feed_ev_next;
+      feed_ev_next = (feed_ev_next + 1) % kFeedRing;
+      if (cudaEventRecord(feed_ev[e], copy) != cudaSuccess) return false;
+      feed_inflight.push_back(e);
+    }
+    return true;
+  }
+  void feed_drop() {
+    feed.clear();
+    feed_next = 0;
+    feed_cancel.clear();
+  }
+
   bool profiling = false;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
@@ -321,6 +366,8 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
                         &ctx->ev_tmp};
   for (auto* e : evs)
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
+  for (auto& e : ctx->feed_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
   if (cudaMemset(ctx->arena + lay.ticket, 0, 64) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
   ctx->slot_base.assign(desc->L, 0);
   ctx->ids_h.resize((size_t)desc->max_batch * desc->K);
@@ -411,6 +458,8 @@ moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg, 
   }
   CK(cudaStreamSynchronize(ctx->copy));
   ctx->pending = Plan();
+  ctx->feed_drop();
+  ctx->cancel_prefetch = cfg->cancel_prefetch != 0;
   ctx->configured = true;
   write_config_out(*ctx->cp, out);
   return MOEPIC_OK;
@@ -511,6 +560,10 @@ static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s) {
 #if defined(__x86_64__)
     __builtin_ia32_pause();
 #endif
+    if ((spins & 0x3F) == 0 && !ctx->feed_pump(moepic_ctx::kFeedDepth)) {
+      ctx->poisoned = true;
+      return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch feed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
     if ((++spins & 0xFFF) == 0) {
       cudaError_t q = cudaStreamQuery(s);
       if (q != cudaSuccess && q != cudaErrorNotReady) {
@@ -567,21 +620,47 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
 }
 
 // Issue the plan's H2D copies into ping-pong half `buf`.
+// Queue the plan's H2D copies (into ping-pong half `buf`) on the feed; a few chunks are issued
+// now, the rest while the host waits for the next routing (or all of them when cancel is off).
 static moepic_status issue_plan(moepic_ctx* ctx, Plan& plan, int buf) {
   plan.buf = buf;
+  ctx->feed_drop();
   if (ctx->ev_step_rec[buf]) CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[buf], 0));
   const int j = plan.target;
   const LayerState& l = ctx->cp->layers[j];
   const uint64_t rb = ctx->rb();
-  for (const auto& it : plan.items) {
+  ctx->feed_cancel.assign(plan.items.size(), 0);
+  for (size_t k = 0; k < plan.items.size(); ++k) {
+    const PlanItem& it = plan.items[k];
     const uint8_t* src = ctx->host_expert(j, it.expert) + (it.full ? 0 : (uint64_t)l.I_top * rb);
-    CK(cudaMemcpyAsync(ctx->plan_ptr(buf, it.buf_row), src, (size_t)it.rows * rb, cudaMemcpyHostToDevice,
-                       ctx->copy));
-    ctx->ctr.h2d_copies++;
+    uint8_t* dst = ctx->plan_ptr(buf, it.buf_row);
+    const size_t total = (size_t)it.rows * rb;
+    for (size_t off = 0; off < total; off += moepic_ctx::kFeedChunk)
+      ctx->feed.push_back({dst + off, src + off, std::min(moepic_ctx::kFeedChunk, total - off), (int32_t)k});
   }
-  CK(cudaEventRecord(ctx->ev_plan[buf], ctx->copy));
-  const uint64_t pb = plan_bytes(plan, (int64_t)rb);
-  ctx->ctr.pcie_prefetch_bytes += pb;
+  ctx->ctr.pcie_prefetch_planned_bytes += plan_bytes(plan, (int64_t)rb);
+  if (!ctx->feed_pump(ctx->cancel_prefetch ? moepic_ctx::kFeedDepth : (size_t)-1)) {
+    ctx->poisoned = true;
+    return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch copy: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  return MOEPIC_OK;
+}
+
+// Routing of the plan's target layer is known: drop the unissued chunks of experts it did not
+// activate, issue everything else, and mark the point the plan's segments wait for.
+static moepic_status finish_plan(moepic_ctx* ctx, const Plan& plan, const StepResult& res) {
+  if (ctx->cancel_prefetch) {
+    std::vector<char> act(ctx->desc.N, 0);
+    for (int e : res.A) act[e] = 1;
+    for (size_t k = 0; k < plan.items.size(); ++k)
+      if (!act[plan.items[k].expert]) ctx->feed_cancel[k] = 1;
+  }
+  if (!ctx->feed_pump((size_t)-1)) {
+    ctx->poisoned = true;
+    return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch copy: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  ctx->feed_drop();
+  CK(cudaEventRecord(ctx->ev_plan[plan.buf], ctx->copy));
   return MOEPIC_OK;
 }
 
@@ -607,6 +686,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   Plan used;
   const bool have_plan = ctx->pending.valid && ctx->pending.target == layer;
   if (have_plan) used = std::move(ctx->pending);
+  else ctx->feed_drop();   // a plan for another layer is abandoned
   ctx->pending = Plan();
   const int buf = have_plan ? used.buf : (ctx->last_buf ^ 1);
 
@@ -618,6 +698,10 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   // ---- control plane (classification, counters, admission)
   StepResult res;
   cp.step(layer, ctx->ids_h.data(), B, have_plan ? &used : nullptr, res);
+  if (have_plan) {
+    st = finish_plan(ctx, used, res);
+    if (st != MOEPIC_OK) return st;
+  }
 
   // token masks per activated expert
   const int K = d.K;
@@ -923,6 +1007,8 @@ void moepic_destroy(moepic_ctx* ctx) {
   if (!ctx) return;
   cudaDeviceSynchronize();
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  for (auto e : ctx->feed_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& pe : ctx->prof) {
     cudaEventDestroy(pe.a);
     cudaEventDestroy(pe.b);
