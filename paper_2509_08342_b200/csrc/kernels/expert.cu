@@ -1,0 +1,344 @@
+// K2 split-expert streaming SwiGLU for decode batches.
+//
+// A segment is a contiguous row range of one expert in the row-interleaved layout
+// [gate_r | up_r | down[:, r]] (6d bytes per row): a cached top (HBM slot), a prefetched or
+// on-demand bottom (ping-pong buffer), a full expert, or a shared expert's rows.  The split-sum
+// identity (y = y_top + y_bottom) means a segment is just a base pointer and a row count.
+//
+// Persistent grid, one CTA per SM (<= 148), CTA c owns launch rows [c R / G, (c+1) R / G).
+// Warp-specialised:
+//   * producer warp (lane 0): streams row tiles of RS rows into a kStages-deep shared-memory ring
+//     with cp.async.bulk (TMA 1-D, L2 evict-first) completing on a `full` mbarrier; reuses a
+//     stage once the 16 consumer warps arrived on its `empty` mbarrier.
+//   * 16 consumer warps: thread t owns CW consecutive columns.  Per tile:
+//       phase 1   partial gate/up dots of the tile's rows over the thread's columns (fp32 FMA),
+//                 warp butterfly, lane 0 stores the warp partials, warp arrives on `red[t&1]`;
+//       phase 2   of the PREVIOUS tile: y_partial[tok][cols] += a[r][tok] * down_r[cols], then the
+//                 warp releases that stage (this work hides the reduction barrier);
+//       finalise  wait `red[t&1]`; every warp sums the 16 warp partials in warp order (fixed,
+//                 deterministic), a = silu(g) * u * w_gate (fp32), broadcast by shuffles.
+//   Per (segment, CTA) partials are written once to the workspace; K3 adds them in a fixed order.
+// Decode has <= 4 tokens per expert (B K / N): CUDA-core FMA at <= 8 flop/byte, HBM-bound; tensor
+// cores are for prefill.
+#include "kernels.hpp"
+#include "device_utils.cuh"
+
+#include <cstdio>
+
+namespace moepic {
+
+namespace {
+
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;
+constexpr int kStagesV2 = 4;
+
+struct Tile {
+  int s;          // segment index
+  int64_t row;    // first launch row
+};
+
+}  // namespace
+
+int k2_rows_per_tile(int d) {
+  if (d > 2048) return 2;
+  if (d > 1024) return 4;
+  if (d > 512) return 8;
+  return 16;
+}
+static int k2_cw(int d) { return d > 2048 ? 8 : 4; }
+int k2_max_tokens(int d) {   // 2 * RS * TB <= 32 reduced values per tile
+  const int rs = k2_rows_per_tile(d);
+  return rs <= 4 ? 4 : 16 / rs;
+}
+size_t k2_smem_bytes(int d) {
+  const int RS = k2_rows_per_tile(d);
+  return (size_t)kStagesV2 * RS * 6 * d + (2 * kStagesV2 + 2) * sizeof(uint64_t) +
+         (size_t)2 * kConsumerWarps * 32 * sizeof(float) + 128;
+}
+
+template <int TB, int CW, int RS>
+__global__ void __maxnreg__(120) k2_split_expert(const __grid_constant__ K2Params p) {
+  static_assert(2 * RS * TB <= 32, "one lane per reduced value");
+  constexpr int NV = 2 * RS * TB;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int d = p.d;
+  const int rowb = 6 * d;
+  const int tileb = RS * rowb;
+  uint8_t* stages = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStagesV2 * tileb);
+  uint64_t* empty = full + kStagesV2;
+  uint64_t* redbar = empty + kStagesV2;
+  float* red = reinterpret_cast<float*>(redbar + 2);   // [2][kConsumerWarps][NV]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t R = p.total_rows;
+  const int64_t G = gridDim.x;
+  const int64_t r0 = k2_row_lo(blockIdx.x, R, G), r1 = k2_row_lo(blockIdx.x + 1, R, G);
+  if (r0 >= r1) return;
+
+  if (tid == 0) {
+    for (int i = 0; i < kStagesV2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumerWarps);
+    }
+    mbar_init(&redbar[0], kConsumerWarps);
+    mbar_init(&redbar[1], kConsumerWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto seg_end = [&](int s) -> int64_t { return (int64_t)p.segs[s].row_begin + p.segs[s].nrows; };
+  Tile start;
+  start.s = 0;
+  while (seg_end(start.s) <= r0) ++start.s;
+  start.row = r0;
+  auto tile_end = [&](const Tile& it) -> int64_t {
+    int64_t e = it.row + RS;
+    const int64_t se = seg_end(it.s);
+    if (e > se) e = se;
+    if (e > r1) e = r1;
+    return e;
+  };
+  auto advance = [&](Tile& it) {
+    const int64_t e = tile_end(it);
+    it.row = e;
+    if (e >= seg_end(it.s)) ++it.s;
+  };
+
+  // ------------------------------------------------------------------ producer warp
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      Tile it = start;
+      for (int n = 0; it.row < r1; ++n) {
+        const int st = n % kStagesV2;
+        if (n >= kStagesV2) mbar_wait(&empty[st], ((n / kStagesV2) - 1) & 1);
+        const int64_t e = tile_end(it);
+        const Seg& sg = p.segs[it.s];
+        const uint32_t bytes = (uint32_t)((e - it.row) * rowb);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(stages + (size_t)st * tileb, sg.base + (it.row - sg.row_begin) * rowb, bytes, &full[st], pol);
+        advance(it);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumer warps
+  const int c0 = tid * CW;               // first owned column
+  const bool owns = c0 < d;
+  float yacc[TB][CW];
+  float hreg[TB][CW];
+  float wgt[TB];
+  float act_prev[RS][TB];
+  int ntok = 0, prev_ntok = 0;
+  int cur = -1, prev_seg = -1, prev_nr = 0;
+  const uint8_t* prev_tile = nullptr;
+  int prev_stage = -1;
+
+  auto load_row = [&](const uint8_t* base, float* f) {
+    if constexpr (CW == 8) unpack8(*reinterpret_cast<const uint4*>(base + c0 * 2), f);
+    else unpack4(*reinterpret_cast<const uint2*>(base + c0 * 2), f);
+  };
+  auto flush = [&](int s, int nt) {
+    const Seg& sg = p.segs[s];
+    const int ci = (int)blockIdx.x - sg.cta_first;
+    float* dst = p.ws + sg.ws_off + (int64_t)ci * nt * d;
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      if (t < nt && owns) {
+        float4* o = reinterpret_cast<float4*>(dst + (int64_t)t * d + c0);
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q)
+          o[q] = make_float4(yacc[t][4 * q], yacc[t][4 * q + 1], yacc[t][4 * q + 2], yacc[t][4 * q + 3]);
+      }
+#pragma unroll
+      for (int c = 0; c < CW; ++c) yacc[t][c] = 0.f;
+    }
+  };
+  auto phase2 = [&]() {   // previous tile: y += a * down_r
+    if (!owns) return;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      if (r < prev_nr) {
+        float dn[CW];
+        load_row(prev_tile + (size_t)r * rowb + 4 * d, dn);
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          const float a = act_prev[r][t];
+#pragma unroll
+          for (int c = 0; c < CW; ++c) yacc[t][c] = fmaf(a, dn[c], yacc[t][c]);
+        }
+      }
+    }
+  };
+#pragma unroll
+  for (int t = 0; t < TB; ++t)
+#pragma unroll
+    for (int c = 0; c < CW; ++c) yacc[t][c] = 0.f;
+
+  Tile it = start;
+  for (int n = 0; it.row < r1; ++n) {
+    const int st = n % kStagesV2;
+    const int s = it.s;
+    const int nr = (int)(tile_end(it) - it.row);
+    if (s != cur) {                      // new segment: its tokens, weights and h columns
+      cur = s;
+      const Seg& sg = p.segs[s];
+      uint32_t m = sg.tok_mask;
+      ntok = 0;
+#pragma unroll
+      for (int t = 0; t < TB; ++t) {
+        wgt[t] = 0.f;
+        int b = -1;
+        if (m) {
+          b = __ffs(m) - 1;
+          m &= m - 1;
+          ++ntok;
+          if (sg.expert >= 0) {
+            for (int k = 0; k < p.K; ++k)
+              if (p.ids[b * p.K + k] == sg.expert) wgt[t] = p.w[b * p.K + k];
+          } else {
+            wgt[t] = 1.f;
+          }
+        }
+        if (b >= 0 && owns) {
+          if constexpr (CW == 8) unpack8(__ldg(reinterpret_cast<const uint4*>(p.h + (size_t)b * d + c0)), hreg[t]);
+          else unpack4(__ldg(reinterpret_cast<const uint2*>(p.h + (size_t)b * d + c0)), hreg[t]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) hreg[t][c] = 0.f;
+        }
+      }
+    }
+    mbar_wait(&full[st], (n / kStagesV2) & 1);
+    const uint8_t* tile = stages + (size_t)st * tileb;
+
+    // ---- phase 1: partial gate / up dots
+    float pv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) pv[v] = 0.f;
+    if (owns) {
+#pragma unroll
+      for (int r = 0; r < RS; ++r) {
+        if (r < nr) {
+          float g[CW], u[CW];
+          load_row(tile + (size_t)r * rowb, g);
+          load_row(tile + (size_t)r * rowb + 2 * d, u);
+#pragma unroll
+          for (int t = 0; t < TB; ++t)
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+              pv[r * TB + t] = fmaf(g[c], hreg[t][c], pv[r * TB + t]);
+              pv[RS * TB + r * TB + t] = fmaf(u[c], hreg[t][c], pv[RS * TB + r * TB + t]);
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) pv[v] += __shfl_xor_sync(0xffffffffu, pv[v], o);
+    float* rb = red + (size_t)(n & 1) * kConsumerWarps * NV;
+    if (lane == 0) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) rb[warp * NV + v] = pv[v];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&redbar[n & 1]);
+
+    // ---- phase 2 of the previous tile, then release its stage
+    if (prev_stage >= 0) {
+      phase2();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[prev_stage]);
+      if (prev_seg != s) flush(prev_seg, prev_ntok);
+    }
+
+    // ---- finalise a = silu(g) * u * w for this tile (every warp, fixed order)
+    mbar_wait(&redbar[n & 1], (n >> 1) & 1);
+    float sum = 0.f;
+    if (lane < NV) {
+#pragma unroll 4
+      for (int w2 = 0; w2 < kConsumerWarps; ++w2) sum += rb[w2 * NV + lane];
+    }
+    const float upart = __shfl_sync(0xffffffffu, sum, (lane + RS * TB) & 31);
+    float a = 0.f;
+    if (lane < RS * TB) {
+      const int r = lane / TB, t = lane - (lane / TB) * TB;
+      float wl = 0.f;
+#pragma unroll
+      for (int q = 0; q < TB; ++q)
+        if (q == t) wl = wgt[q];
+      if (r < nr && t < ntok) a = sum / (1.f + __expf(-sum)) * upart * wl;
+    }
+#pragma unroll
+    for (int r = 0; r < RS; ++r)
+#pragma unroll
+      for (int t = 0; t < TB; ++t) act_prev[r][t] = __shfl_sync(0xffffffffu, a, r * TB + t);
+
+    prev_stage = st;
+    prev_tile = tile;
+    prev_nr = nr;
+    prev_seg = s;
+    prev_ntok = ntok;
+    advance(it);
+  }
+  if (prev_stage >= 0) {
+    phase2();
+    flush(prev_seg, prev_ntok);
+  }
+}
+
+template <int TB, int CW, int RS>
+static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
+  k2_split_expert<TB, CW, RS><<<grid, kThreads, k2_smem_bytes(p.d), s>>>(p);
+}
+
+template <int CW, int RS>
+static void k2_dispatch_tb(const K2Params& p, int grid, int tb, cudaStream_t s) {
+  switch (tb) {
+    case 1: k2_launch_t<1, CW, RS>(p, grid, s); break;
+    case 2:
+      if constexpr (RS <= 8) k2_launch_t<2, CW, RS>(p, grid, s);
+      break;
+    default:
+      if constexpr (RS <= 4) k2_launch_t<4, CW, RS>(p, grid, s);
+      break;
+  }
+}
+
+void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s) {
+  const int rs = k2_rows_per_tile(p.d);
+  if (k2_cw(p.d) == 8) k2_dispatch_tb<8, 2>(p, grid, tb, s);
+  else if (rs == 4) k2_dispatch_tb<4, 4>(p, grid, tb, s);
+  else if (rs == 8) k2_dispatch_tb<4, 8>(p, grid, tb, s);
+  else k2_dispatch_tb<4, 16>(p, grid, tb, s);
+}
+
+template <int TB, int CW, int RS>
+static cudaError_t k2_attr() {
+  return cudaFuncSetAttribute(k2_split_expert<TB, CW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              220 * 1024);
+}
+
+bool kernels_init(char* err, size_t errlen) {
+  cudaError_t e = cudaSuccess;
+  cudaError_t r;
+#define MOEPIC_ATTR(TB, CW, RS) \
+  if ((r = k2_attr<TB, CW, RS>()) != cudaSuccess) e = r;
+  MOEPIC_ATTR(1, 8, 2) MOEPIC_ATTR(2, 8, 2) MOEPIC_ATTR(4, 8, 2)
+  MOEPIC_ATTR(1, 4, 4) MOEPIC_ATTR(2, 4, 4) MOEPIC_ATTR(4, 4, 4)
+  MOEPIC_ATTR(1, 4, 8) MOEPIC_ATTR(2, 4, 8)
+  MOEPIC_ATTR(1, 4, 16)
+#undef MOEPIC_ATTR
+  if (e != cudaSuccess) {
+    snprintf(err, errlen, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return false;
+  }
+  return true;
+}
+
+}  // namespace moepic

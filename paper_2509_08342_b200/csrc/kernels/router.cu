@@ -1,0 +1,168 @@
+// K1 router + next-layer predictor (Eq. 2; Eq. 3).
+//
+// One warp per (matrix, token, expert) logit in fp64 canonical order C.R (R1): chunk
+// c of 8 consecutive k is lane c%32's; lanes add exact bf16*bf16 products in increasing k;
+// xor-butterfly 16,8,4,2,1.  The last CTA (ticket) selects the top-K per token by (logit desc,
+// id asc) with warp-shuffle argmax rounds, computes the Eq. 2 weights, ranks the next layer's
+// experts (reading Q9) and publishes ids / weights / ranking to device memory and to the
+// mapped-pinned mailbox (__threadfence_system, then seq).
+#include "kernels.hpp"
+#include "device_utils.cuh"
+
+#include <cstdio>
+
+namespace moepic {
+
+// ============================================================== K1 router
+struct Key {  // (value desc, id asc)
+  double v;
+  int id;
+};
+__device__ __forceinline__ bool key_better(double av, int aid, double bv, int bid) {
+  return av > bv || (av == bv && aid < bid);
+}
+
+// top-K of row[0..N) by (value desc, id asc) using one warp; writes ids_out[0..K) on lane 0
+// and returns on every lane the selection bitmap of this lane's experts.
+__device__ void warp_topk(const double* row, int N, int K, int* ids_out, unsigned* taken_bits) {
+  const int lane = threadIdx.x & 31;
+  unsigned taken = 0;  // bit q <-> expert lane + 32 q
+  for (int r = 0; r < K; ++r) {
+    double bv = -INFINITY;
+    int bid = 0x7fffffff;
+    for (int q = 0, j = lane; j < N; ++q, j += 32) {
+      if (taken & (1u << q)) continue;
+      double v = row[j];
+      if (key_better(v, j, bv, bid)) { bv = v; bid = j; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (key_better(ov, oid, bv, bid)) { bv = ov; bid = oid; }
+    }
+    if ((bid & 31) == lane) taken |= 1u << (bid >> 5);
+    if (lane == 0) ids_out[r] = bid;
+  }
+  *taken_bits = taken;
+}
+
+__global__ void __launch_bounds__(256) k1_router(RouterParams p) {
+  __shared__ int s_last;
+  __shared__ int s_cnt[kMaxN];
+  __shared__ double s_max[kMaxN];
+  __shared__ int s_topk[8][64];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int BN = p.B * p.N;
+  const int total = BN * 2;
+  const int n_chunks = p.d >> 3;
+
+  // ---- phase 1: one warp per (matrix, token, expert) logit
+  const int gw = blockIdx.x * nwarps + warp;
+  if (gw < total) {
+    const int m = gw / BN;
+    const int rem = gw - m * BN;
+    const int b = rem / p.N;
+    const int j = rem - b * p.N;
+    const uint16_t* W = m == 0 ? p.W0 : p.W1;
+    if (W != nullptr) {
+      const uint4* hv = reinterpret_cast<const uint4*>(p.h + (size_t)b * p.d);
+      const uint4* wv = reinterpret_cast<const uint4*>(W + (size_t)j * p.d);
+      double acc = 0.0;
+      for (int c = lane; c < n_chunks; c += 32) {
+        uint4 a = __ldg(hv + c), w = __ldg(wv + c);
+        float fa[8], fw[8];
+        unpack8(a, fa);
+        unpack8(w, fw);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc += (double)fa[e] * (double)fw[e];  // exact product
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) p.logits[(size_t)m * BN + rem] = acc;
+    }
+  }
+  // ---- last CTA does the selection
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(p.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double* L0 = p.logits;
+  const double* L1 = p.logits + BN;
+  if (p.W0 != nullptr) {
+    for (int b = warp; b < p.B; b += nwarps) {
+      unsigned bits;
+      warp_topk(L0 + (size_t)b * p.N, p.N, p.K, s_topk[warp], &bits);
+      __syncwarp();
+      if (lane == 0) {
+        const double* row = L0 + (size_t)b * p.N;
+        double mx = row[s_topk[warp][0]];
+        double den = 0.0;
+        if (p.renorm) {
+          for (int k = 0; k < p.K; ++k) den += exp(row[s_topk[warp][k]] - mx);
+        } else {
+          for (int j = 0; j < p.N; ++j) den += exp(row[j] - mx);
+        }
+        for (int k = 0; k < p.K; ++k) {
+          int e = s_topk[warp][k];
+          float wk = (float)(exp(row[e] - mx) / den);
+          p.ids[b * p.K + k] = e;
+          p.w[b * p.K + k] = wk;
+          p.mb_ids[b * p.K + k] = e;
+          p.mb_w[b * p.K + k] = wk;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (p.W1 != nullptr) {
+    for (int j = threadIdx.x; j < p.N; j += blockDim.x) {
+      s_cnt[j] = 0;
+      double mx = -INFINITY;
+      for (int b = 0; b < p.B; ++b) mx = fmax(mx, L1[(size_t)b * p.N + j]);
+      s_max[j] = mx;
+    }
+    __syncthreads();
+    for (int b = warp; b < p.B; b += nwarps) {
+      unsigned bits;
+      warp_topk(L1 + (size_t)b * p.N, p.N, p.K, s_topk[warp], &bits);
+      for (int q = 0, j = lane; j < p.N; ++q, j += 32)
+        if (bits & (1u << q)) atomicAdd(&s_cnt[j], 1);
+    }
+    __syncthreads();
+    // rank_j = #{j' : key(j') before key(j)}, key = (count desc, max logit desc, id asc)
+    for (int j = threadIdx.x; j < p.N; j += blockDim.x) {
+      int r = 0;
+      const int cj = s_cnt[j];
+      const double mj = s_max[j];
+      for (int o = 0; o < p.N; ++o) {
+        const int co = s_cnt[o];
+        const double mo = s_max[o];
+        r += (co > cj) || (co == cj && (mo > mj || (mo == mj && o < j)));
+      }
+      p.ranking[r] = j;
+      p.mb_rank[r] = j;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *p.ticket = 0u;
+    __threadfence_system();
+    *p.mb_seq = p.seq;
+    __threadfence_system();
+  }
+}
+
+void launch_router(const RouterParams& p, cudaStream_t s) {
+  const int warps = 2 * p.B * p.N;
+  const int grid = (warps + 7) / 8;
+  k1_router<<<grid, 256, 0, s>>>(p);
+}
+
+}  // namespace moepic
