@@ -38,7 +38,7 @@ METRIC = "MoE-layer decode throughput at 50% expert VRAM budget (tokens/s throug
 CONFIGS = {
     # name: (shape, L, L_host, B, v_e fraction, theta)
     "mixtral": dict(shape="mixtral", L=32, L_host=2, B=1, budget=0.5, theta=0.5),
-    "qwen3": dict(shape="qwen3", L=48, L_host=4, B=1, budget=0.5, theta=0.5),
+    "qwen3": dict(shape="qwen3", L=48, L_host=4, B=1, budget=0.5, theta=0.5, adaptive=True),
     "deepseek": dict(shape="deepseek", L=26, L_host=4, B=1, budget=0.5, theta=0.5),
     "toy": dict(shape="toy", L=2, L_host=2, B=1, budget=0.25, theta=0.5),
 }
@@ -166,28 +166,48 @@ def run_ours(args, log):
     ctx, desc, S, v_e, keep = build_model(api, synth, torch, cfg, rank, world, max_batch=cfg["B"], log=log)
     L, B = cfg["L"], cfg["B"]
     t0 = time.time()
-    ctx.configure(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
+    base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
+    ctx.configure(**base_cfg)
     log(f"[bench] configure (re-layout {v_e:.0f} tops) {time.time() - t0:.1f}s")
-    T = args.warmup + args.steps
-    H = synth.hidden_states(1, T + args.e2e_steps + 1, L, S.d).to("cuda")  # [T][L][d]
+    adapt_tokens = 2 * args.tau if cfg.get("adaptive") else 0
+    T = adapt_tokens + args.warmup + args.steps
+    # token t, layer i uses rows [t*B, (t+1)*B) of a [T*B][L][d] organic hidden-state process
+    # stored [L][tokens][d] so every per-layer batch slice is a contiguous [B][d] block
+    H = synth.hidden_states(1, (T + args.e2e_steps + 1) * B, L, S.d).permute(1, 0, 2).contiguous().to("cuda")
     y = torch.empty(B, S.d, dtype=torch.float32, device="cuda")
     stream = torch.cuda.Stream()
     F = api.M.FUSE_PREDICT
 
     def token(t):
         for i in range(L):
-            ctx.layer_forward(i, H[t, i][None], y, stream=stream, flags=F, trace=False)
-            if world > 1:
-                pass  # combine: all-reduce of partial y (below, per layer) — see DESIGN.md §EP
+            ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=F, trace=False)
 
     def token_ep(t):
         for i in range(L):
-            ctx.layer_forward(i, H[t, i][None], y, stream=stream, flags=F, trace=False)
+            ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=F, trace=False)
             with torch.cuda.stream(stream):
-                dist.all_reduce(y)
+                dist.all_reduce(y)      # EP combine: sum of per-rank partial outputs
 
     step = token_ep if world > 1 else token
-    for t in range(args.warmup):
+    solved = None
+    if adapt_tokens:
+        # Alg. 1 outer loop: run 2 tau tokens on the uniform theta = 0.5 layout, profile
+        # T_moe on this GPU and T_load^exp = U_e / PCIe, then reconfigure with the solver.
+        ctx.profile(True)
+        for t in range(adapt_tokens):
+            step(t)
+        torch.cuda.synchronize()
+        k2w = ctx.profile_read(api.M.KERNEL_EXPERT)
+        ctx.profile(False)
+        U_e = 6 * S.d * S.I
+        t_load = U_e / (pcie * 1e9) * 1e3                          # ms per full expert
+        t_moe = k2w["total_ms"] / (adapt_tokens * L)               # ms of expert compute per layer-step
+        t0 = time.time()
+        solved = ctx.configure(use_solver=True, t_att=0.0, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
+                               zeta=0.01, **{k: v for k, v in base_cfg.items() if k != "theta_i"})
+        log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(solved['theta_eff_i']):.2f}.."
+            f"{max(solved['theta_eff_i']):.2f}, C {min(solved['C_i'])}..{max(solved['C_i'])}")
+    for t in range(adapt_tokens, adapt_tokens + args.warmup):
         step(t)
     torch.cuda.synchronize()
     if dist:
@@ -201,7 +221,7 @@ def run_ours(args, log):
     torch.cuda.synchronize()
     ev0.record(stream)
     per_tok = []
-    for t in range(args.warmup, T):
+    for t in range(adapt_tokens + args.warmup, T):
         a = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         step(t)
@@ -230,7 +250,7 @@ def run_ours(args, log):
     # ---- end to end through the host-buffer API (pinned staging inside the library)
     e2e = None
     if args.e2e_steps > 0:
-        Hh = [[synth.bf16_bits(H[t, i][None].cpu()) for i in range(L)] for t in range(T, T + args.e2e_steps)]
+        Hh = [[synth.bf16_bits(H[i, t * B:(t + 1) * B].cpu()) for i in range(L)] for t in range(T, T + args.e2e_steps)]
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -258,6 +278,9 @@ def run_ours(args, log):
                    "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
                    "global_batch": B, "seq_len": 1, "parallelism": f"ep{world}" if world > 1 else "single",
                    "v_e_experts": v_e, "theta": cfg["theta"], "policy": "LCP", "y_cap": S.K * B,
+                   "alg1": None if solved is None else {"tau_tokens": args.tau, "theta_eff_min": min(solved["theta_eff_i"]),
+                                                        "theta_eff_max": max(solved["theta_eff_i"]),
+                                                        "C_min": min(solved["C_i"]), "C_max": max(solved["C_i"])},
                    "l2": "inputs larger than L2 (>=700 MB of expert rows streamed per layer)"},
         "layer_latency_us": {"mean": round(layer_us, 2),
                              "p50_token_ms": round(statistics.median(tok_ms), 3),
@@ -380,8 +403,15 @@ def main():
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's decode batch")
+    ap.add_argument("--tau", type=int, default=128, help="tokens per Alg. 1 period (adaptive configs)")
+    ap.add_argument("--no-adapt", action="store_true", help="keep the uniform theta = 0.5 layout")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.batch:
+        CONFIGS[args.config]["B"] = args.batch
+    if args.no_adapt:
+        CONFIGS[args.config]["adaptive"] = False
     rank = int(os.environ.get("RANK", "0"))
     log = (lambda *a: print(*a, file=sys.stderr, flush=True))
     if args.impl == "reference":

@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kThreads = kConsumers + 32;
+constexpr int kThreads = kConsumers;   // 4 warps per SM sub-partition -> 128 registers / thread
 constexpr int kStagesV2 = 4;
 
 struct Tile {
@@ -59,7 +59,7 @@ size_t k2_smem_bytes(int d) {
 }
 
 template <int TB, int CW, int RS>
-__global__ void __maxnreg__(120) k2_split_expert(const __grid_constant__ K2Params p) {
+__global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_constant__ K2Params p) {
   static_assert(2 * RS * TB <= 32, "one lane per reduced value");
   constexpr int NV = 2 * RS * TB;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -107,23 +107,26 @@ __global__ void __maxnreg__(120) k2_split_expert(const __grid_constant__ K2Param
     if (e >= seg_end(it.s)) ++it.s;
   };
 
-  // ------------------------------------------------------------------ producer warp
-  if (warp == kConsumerWarps) {
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      Tile it = start;
-      for (int n = 0; it.row < r1; ++n) {
-        const int st = n % kStagesV2;
-        if (n >= kStagesV2) mbar_wait(&empty[st], ((n / kStagesV2) - 1) & 1);
-        const int64_t e = tile_end(it);
-        const Seg& sg = p.segs[it.s];
-        const uint32_t bytes = (uint32_t)((e - it.row) * rowb);
-        mbar_expect_tx(&full[st], bytes);
-        bulk_g2s(stages + (size_t)st * tileb, sg.base + (it.row - sg.row_begin) * rowb, bytes, &full[st], pol);
-        advance(it);
-      }
-    }
-    return;
+  // ------------------------------------------------------------------ TMA producer (warp 0 lane 0)
+  // Prologue fills every stage; afterwards tile n-1+S is issued into tile n-1's stage as soon as
+  // all warps released it (in iteration n, right after warp 0's own release).
+  const bool producer = tid == 0;
+  uint64_t pol = 0;
+  Tile pit = start;
+  int pn = 0;   // next tile index to issue
+  auto issue = [&]() {
+    const int pst = pn % kStagesV2;
+    const int64_t e = tile_end(pit);
+    const Seg& sg = p.segs[pit.s];
+    const uint32_t bytes = (uint32_t)((e - pit.row) * rowb);
+    mbar_expect_tx(&full[pst], bytes);
+    bulk_g2s(stages + (size_t)pst * tileb, sg.base + (pit.row - sg.row_begin) * rowb, bytes, &full[pst], pol);
+    advance(pit);
+    ++pn;
+  };
+  if (producer) {
+    pol = evict_first_policy();
+    while (pn < kStagesV2 && pit.row < r1) issue();
   }
 
   // ------------------------------------------------------------------ consumer warps
@@ -254,6 +257,10 @@ __global__ void __maxnreg__(120) k2_split_expert(const __grid_constant__ K2Param
       phase2();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[prev_stage]);
+      if (producer && pit.row < r1) {   // refill tile n-1's stage with tile n-1+S
+        mbar_wait(&empty[prev_stage], ((n - 1) / kStagesV2) & 1);
+        issue();
+      }
       if (prev_seg != s) flush(prev_seg, prev_ntok);
     }
 
