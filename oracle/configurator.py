@@ -37,11 +37,12 @@ class SubResult:
     m: float
     T: float
     window_next: float
+    Y: int = 0          # prefetch operations that fit the window at C* (Eq. 10)
 
 
 def solve_subproblem(st, V: float, W: float, K: int, N: int, U_b: float,
                      t_load: float, t_cexp: float, t_moe: float, t_att: float) -> SubResult:
-    best_C, best_theta, best_m = None, 0.0, 0.0
+    best_C, best_theta, best_m, best_Y = None, 0.0, 0.0, 0
     C_lo = max(1, int(math.ceil(V - 1e-9)))
     if C_lo > N:
         C_lo = N
@@ -52,6 +53,7 @@ def solve_subproblem(st, V: float, W: float, K: int, N: int, U_b: float,
         m = (K * st.H(C)) * theta
         cum = 0.0
         fcum = 0.0
+        Y = 0
         for y in range(1, N + 1):
             f = 1.0 - st.PH(y, C) * theta
             c = f * t_load
@@ -60,16 +62,17 @@ def solve_subproblem(st, V: float, W: float, K: int, N: int, U_b: float,
             cum = cum + c
             fcum = fcum + f
             m = m + f * st.P(y)
+            Y = y
         if best_C is None or m > best_m:
-            best_C, best_theta, best_m = C, theta, m
+            best_C, best_theta, best_m, best_Y = C, theta, m, Y
     m = best_m
     T = max(0.0, (K - m) * t_load - m * t_cexp)
     w_next = (t_moe - min(m * t_cexp, (K - m) * t_load)) + t_att
-    return SubResult(best_C, best_theta, m, T, w_next)
+    return SubResult(best_C, best_theta, m, T, w_next, best_Y)
 
 
-def expert_split(stats, V, K, N, U_b, t_att, t_moe, t_head, t_load):
-    """Function ExpertSplit.  Returns (T[], theta[], C[])."""
+def expert_split(stats, V, K, N, U_b, t_att, t_moe, t_head, t_load, Ys=None):
+    """Function ExpertSplit.  Returns (T[], theta[], C[]); fills Ys with Y_i if given."""
     t_cexp = t_moe / K
     W = t_head + t_att
     Ts, ths, Cs = [], [], []
@@ -78,17 +81,26 @@ def expert_split(stats, V, K, N, U_b, t_att, t_moe, t_head, t_load):
         Ts.append(r.T)
         ths.append(r.theta)
         Cs.append(r.C)
+        if Ys is not None:
+            Ys.append(r.Y)
         W = r.window_next
     return Ts, ths, Cs
 
 
 def vram_allocation(stats, V_init, V_e, zeta, K, N, U_b, t_att, t_moe, t_head, t_load):
-    """Function VramAllocation.  Returns (V[], theta[], C[], iterations, converged)."""
+    """Function VramAllocation.  Returns (V[], theta[], C[], iterations, converged).
+    The final ExpertSplit's per-layer Y (prefetches fitting the window, Eq. 10) is available as
+    vram_allocation.last_Y after the call."""
     L = len(V_init)
     delta = zeta * V_e
     V = list(V_init)
     cap = 10 * L * int(math.ceil(1.0 / zeta))
     es = lambda vv: expert_split(stats, vv, K, N, U_b, t_att, t_moe, t_head, t_load)
+
+    def _ys(vv):
+        ys = []
+        expert_split(stats, vv, K, N, U_b, t_att, t_moe, t_head, t_load, ys)
+        return ys
     for it in range(cap):
         T1, th1, C1 = es(V)
         T2, _, _ = es([v + delta for v in V])
@@ -104,6 +116,7 @@ def vram_allocation(stats, V_init, V_e, zeta, K, N, U_b, t_att, t_moe, t_head, t
             if i2 < 0 or T3[i] - T1[i] < T3[i2] - T1[i2]:
                 i2 = i
         if i2 < 0:
+            vram_allocation.last_Y = _ys(V)
             return V, th1, C1, it, True
         Vn = list(V)
         Vn[i1] = Vn[i1] + delta
@@ -115,7 +128,9 @@ def vram_allocation(stats, V_init, V_e, zeta, K, N, U_b, t_att, t_moe, t_head, t
         for i in range(L):
             s = s + (T4[i] - T1[i])
         if s >= 0.0:
+            vram_allocation.last_Y = _ys(V)
             return V, th1, C1, it, True
         V = Vn
     T, th, C = es(V)
+    vram_allocation.last_Y = _ys(V)
     return V, th, C, cap, False

@@ -95,6 +95,7 @@ class OracleEngine:
         self.C = [0] * L
         self.I_top = [0] * L
         self.V = None
+        self.Y = None
         self.stats = [LayerStats(N, K) for _ in range(L)]
         self.rnd = [0] * L
         self.cfg = None
@@ -129,7 +130,9 @@ class OracleEngine:
                                              cfg.t_att, cfg.t_moe, cfg.t_head, cfg.t_load_exp)
             thetas = th
             Cs = C
+            self.Y = list(vram_allocation.last_Y)   # Eq. 10's Y caps the planner (reading Q27)
         else:
+            self.Y = None
             V = list(cfg.v_i) if cfg.v_i is not None else [cfg.v_e / L] * L
             thetas = list(cfg.theta_i) if cfg.theta_i is not None else [0.5] * L
             s = 0.0
@@ -182,6 +185,8 @@ class OracleEngine:
             return Plan(j, [], ranking)
         cap_rows = self.U_b * self.I
         ycap = self.N if cfg.y_cap_i is None else cfg.y_cap_i[j]
+        if self.Y is not None:
+            ycap = min(ycap, self.Y[j])
         items, used = [], 0
         for e in ranking:
             e = int(e)

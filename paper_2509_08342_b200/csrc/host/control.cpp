@@ -106,6 +106,7 @@ SubResult solve_subproblem(const Stats& st, double V, double W, int K, int N, do
   int C_lo = std::max(1, (int)std::ceil(V - 1e-9));
   if (C_lo > N) C_lo = N;
   bool have = false;
+  int best_Y = 0;
   int best_C = 0;
   double best_theta = 0.0, best_m = 0.0;
   const double Kd = (double)K;
@@ -114,6 +115,7 @@ SubResult solve_subproblem(const Stats& st, double V, double W, int K, int N, do
     if (theta > 1.0) theta = 1.0;
     double m = (Kd * st.H(C)) * theta;
     double cum = 0.0, fcum = 0.0;
+    int Y = 0;
     for (int y = 1; y <= N; ++y) {
       double f = 1.0 - st.PH(y, C) * theta;
       double c = f * t_load;
@@ -121,8 +123,9 @@ SubResult solve_subproblem(const Stats& st, double V, double W, int K, int N, do
       cum = cum + c;
       fcum = fcum + f;
       m = m + f * st.P(y);
+      Y = y;
     }
-    if (!have || m > best_m) { have = true; best_C = C; best_theta = theta; best_m = m; }
+    if (!have || m > best_m) { have = true; best_C = C; best_theta = theta; best_m = m; best_Y = Y; }
   }
   SubResult r;
   r.C = best_C;
@@ -131,12 +134,15 @@ SubResult solve_subproblem(const Stats& st, double V, double W, int K, int N, do
   double x = (Kd - best_m) * t_load - best_m * t_cexp;
   r.T = std::max(0.0, x);
   r.window_next = (t_moe - std::min(best_m * t_cexp, (Kd - best_m) * t_load)) + t_att;
+  r.Y = best_Y;
   return r;
 }
 
 void expert_split(const std::vector<Stats>& st, const std::vector<double>& V, int K, int N,
                   double U_b, double t_att, double t_moe, double t_head, double t_load,
-                  std::vector<double>& T, std::vector<double>& theta, std::vector<int>& C) {
+                  std::vector<double>& T, std::vector<double>& theta, std::vector<int>& C,
+                  std::vector<int>* Y) {
+  if (Y) Y->assign(V.size(), 0);
   const double t_cexp = t_moe / (double)K;
   double W = t_head + t_att;
   size_t L = V.size();
@@ -144,13 +150,21 @@ void expert_split(const std::vector<Stats>& st, const std::vector<double>& V, in
   for (size_t i = 0; i < L; ++i) {
     SubResult r = solve_subproblem(st[i], V[i], W, K, N, U_b, t_load, t_cexp, t_moe, t_att);
     T[i] = r.T; theta[i] = r.theta; C[i] = r.C;
+    if (Y) (*Y)[i] = r.Y;
     W = r.window_next;
   }
 }
 
 int vram_allocation(const std::vector<Stats>& st, std::vector<double>& V, double V_e, double zeta,
                     int K, int N, double U_b, double t_att, double t_moe, double t_head,
-                    double t_load, std::vector<double>& theta, std::vector<int>& C, bool& converged) {
+                    double t_load, std::vector<double>& theta, std::vector<int>& C, bool& converged,
+                    std::vector<int>* Y) {
+  auto ys = [&](const std::vector<double>& vv) {
+    if (!Y) return;
+    std::vector<double> t_, th_;
+    std::vector<int> c_;
+    expert_split(st, vv, K, N, U_b, t_att, t_moe, t_head, t_load, t_, th_, c_, Y);
+  };
   const int L = (int)V.size();
   const double delta = zeta * V_e;
   const int cap = 10 * L * (int)std::ceil(1.0 / zeta);
@@ -169,7 +183,7 @@ int vram_allocation(const std::vector<Stats>& st, std::vector<double>& V, double
       if (i == i1 || V[i] + 1e-9 < delta) continue;
       if (i2 < 0 || T3[i] - T1[i] < T3[i2] - T1[i2]) i2 = i;
     }
-    if (i2 < 0) { theta = th; C = C1; converged = true; return it; }
+    if (i2 < 0) { theta = th; C = C1; converged = true; ys(V); return it; }
     Vn = V;
     Vn[i1] = Vn[i1] + delta;
     Vn[i2] = Vn[i2] - delta;
@@ -177,10 +191,10 @@ int vram_allocation(const std::vector<Stats>& st, std::vector<double>& V, double
     expert_split(st, Vn, K, N, U_b, t_att, t_moe, t_head, t_load, T4, th_tmp, c_tmp);
     double s = 0.0;
     for (int i = 0; i < L; ++i) s = s + (T4[i] - T1[i]);
-    if (s >= 0.0) { theta = th; C = C1; converged = true; return it; }
+    if (s >= 0.0) { theta = th; C = C1; converged = true; ys(V); return it; }
     V = Vn;
   }
-  expert_split(st, V, K, N, U_b, t_att, t_moe, t_head, t_load, T1, theta, C);
+  expert_split(st, V, K, N, U_b, t_att, t_moe, t_head, t_load, T1, theta, C, Y);
   converged = false;
   return cap;
 }
@@ -222,6 +236,7 @@ std::string ControlPlane::configure(const CacheParams& p, uint64_t slot_pool_row
   std::vector<double> Vnew;
   std::vector<double> thetas;
   std::vector<int> Cs(L);
+  std::vector<int> Ys;   // Eq. 10's Y per layer (solver only): caps the planner (reading Q27)
   if (p.use_solver) {
     for (int i = 0; i < L; ++i)
       if (layers[i].st.q == 0) return "empty accumulator (layer " + std::to_string(i) + ")";
@@ -233,7 +248,7 @@ std::string ControlPlane::configure(const CacheParams& p, uint64_t slot_pool_row
     for (int i = 0; i < L; ++i) st[i] = layers[i].st;
     bool conv = false;
     vram_allocation(st, Vnew, p.v_e, p.zeta, K, N, (double)U_b, p.t_att, p.t_moe, p.t_head, p.t_load,
-                    thetas, Cs, conv);
+                    thetas, Cs, conv, &Ys);
   } else {
     Vnew = p.v_i.empty() ? std::vector<double>(L, p.v_e / (double)L) : p.v_i;
     thetas = p.theta_i.empty() ? std::vector<double>(L, 0.5) : p.theta_i;
@@ -266,6 +281,7 @@ std::string ControlPlane::configure(const CacheParams& p, uint64_t slot_pool_row
     l.C = Cs[i];
     l.I_top = Itop[i];
     l.V = Vnew[i];
+    l.Y = Ys.empty() ? -1 : Ys[i];
     std::fill(l.slot_of.begin(), l.slot_of.end(), -1);
     l.slot_expert.assign(std::max(0, l.C), -1);
     l.n_cached = 0;
@@ -409,7 +425,8 @@ void ControlPlane::make_plan(int j, const int32_t* ranking, Plan& out) const {
   if (!cfg.prefetch) return;
   const LayerState& l = layers[j];
   const int64_t cap_rows = (int64_t)U_b * I;
-  const int ycap = cfg.y_cap.empty() ? N : cfg.y_cap[j];
+  int ycap = cfg.y_cap.empty() ? N : cfg.y_cap[j];
+  if (l.Y >= 0) ycap = std::min(ycap, l.Y);
   int64_t used = 0;
   for (int y = 0; y < N; ++y) {
     int e = ranking[y];

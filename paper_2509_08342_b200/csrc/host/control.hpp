@@ -48,16 +48,18 @@ struct Stats {
 };
 
 // ---------------------------------------------------------------- configurator (Alg. 1)
-struct SubResult { int C; double theta, m, T, window_next; };
+struct SubResult { int C; double theta, m, T, window_next; int Y; };   // Y: prefetches fitting the window
 SubResult solve_subproblem(const Stats& st, double V, double W, int K, int N, double U_b,
                            double t_load, double t_cexp, double t_moe, double t_att);
 void expert_split(const std::vector<Stats>& st, const std::vector<double>& V, int K, int N,
                   double U_b, double t_att, double t_moe, double t_head, double t_load,
-                  std::vector<double>& T, std::vector<double>& theta, std::vector<int>& C);
+                  std::vector<double>& T, std::vector<double>& theta, std::vector<int>& C,
+                  std::vector<int>* Y = nullptr);
 // returns iterations; V is updated in place
 int vram_allocation(const std::vector<Stats>& st, std::vector<double>& V, double V_e, double zeta,
                     int K, int N, double U_b, double t_att, double t_moe, double t_head,
-                    double t_load, std::vector<double>& theta, std::vector<int>& C, bool& converged);
+                    double t_load, std::vector<double>& theta, std::vector<int>& C, bool& converged,
+                    std::vector<int>* Y = nullptr);
 
 // ---------------------------------------------------------------- cache + planner state
 struct PlanItem {
@@ -83,6 +85,7 @@ struct LayerState {
   int n_cached = 0;
   int C = 0, I_top = 0;
   double V = 0.0;
+  int Y = -1;        // Alg. 1's prefetch count (Eq. 10) when the config came from the solver
   uint64_t rnd = 0;
   Stats st;
   bool cache_on() const { return C > 0 && I_top > 0; }

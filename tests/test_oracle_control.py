@@ -94,7 +94,7 @@ def test_subproblem_prefetch_only_vector():
     K, N = 4, 8
     st = FakeStats(N, lambda C: 0.3, lambda y: 1.0 if y <= K else 0.0, lambda y, C: 0.5)
     r = CF.solve_subproblem(st, 0.0, 2 * 40.0, K, N, float(K), 40.0, 10.0, 40.0, 15.0)
-    assert r.m == 2.0 and r.C == 1
+    assert r.m == 2.0 and r.C == 1 and r.Y == 2
 
 
 def test_subproblem_full_hit_vector():
