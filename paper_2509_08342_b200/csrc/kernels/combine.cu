@@ -8,7 +8,17 @@ namespace moepic {
 // CTA (x, b): 32 float4 columns of token b; warp w sums chunks w, w+8, ... of every segment
 // serving b (lane = column), then the 8 warp partials are added in warp order.  Fixed order
 // everywhere -> deterministic.
-__global__ void __launch_bounds__(256) k3_combine(const __grid_constant__ CombineParams p) {
+template <int CAP>
+struct CombineParamsCap {
+  float* y;
+  const uint16_t* h;
+  const float* ws;
+  int B, d, residual, nsegs;
+  CombineSeg segs[CAP];
+};
+
+template <class P>
+__global__ void __launch_bounds__(256) k3_combine(const __grid_constant__ P p) {
   __shared__ float4 red[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.y;
@@ -59,9 +69,21 @@ __global__ void __launch_bounds__(256) k3_combine(const __grid_constant__ Combin
   }
 }
 
-void launch_combine(const CombineParams& p, cudaStream_t s) {
+// parameter block sized to the step (see expert.cu: launch commands cross the busy PCIe link)
+template <int CAP>
+static void launch_cap(const CombineParams& p, cudaStream_t s) {
+  CombineParamsCap<CAP> q;
+  q.y = p.y; q.h = p.h; q.ws = p.ws;
+  q.B = p.B; q.d = p.d; q.residual = p.residual; q.nsegs = p.nsegs;
+  for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   dim3 grid((unsigned)((p.d / 4 + 31) / 32), (unsigned)p.B);
-  k3_combine<<<grid, 256, 0, s>>>(p);
+  k3_combine<CombineParamsCap<CAP>><<<grid, 256, 0, s>>>(q);
+}
+
+void launch_combine(const CombineParams& p, cudaStream_t s) {
+  if (p.nsegs <= 16) launch_cap<16>(p, s);
+  else if (p.nsegs <= 128) launch_cap<128>(p, s);
+  else launch_cap<kMaxStepSegs>(p, s);
 }
 
 }  // namespace moepic

@@ -58,8 +58,8 @@ size_t k2_smem_bytes(int d) {
          (size_t)2 * kConsumerWarps * 32 * sizeof(float) + 128;
 }
 
-template <int TB, int CW, int RS>
-__global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_constant__ K2Params p) {
+template <int TB, int CW, int RS, class P>
+__global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_constant__ P p) {
   static_assert(2 * RS * TB <= 32, "one lane per reduced value");
   constexpr int NV = 2 * RS * TB;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -299,20 +299,44 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   }
 }
 
-template <int TB, int CW, int RS>
+// The kernel parameter block is sized to the launch: kernel arguments travel in the launch
+// command the GPU front-end fetches over PCIe, which the prefetch stream keeps saturated.
+template <int CAP>
+struct K2ParamsCap {
+  const uint16_t* h;
+  const int32_t* ids;
+  const float* w;
+  float* ws;
+  int64_t total_rows;
+  int d, K, nsegs;
+  Seg segs[CAP];
+};
+
+template <int TB, int CW, int RS, int CAP>
 static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
-  k2_split_expert<TB, CW, RS><<<grid, kThreads, k2_smem_bytes(p.d), s>>>(p);
+  K2ParamsCap<CAP> q;
+  q.h = p.h; q.ids = p.ids; q.w = p.w; q.ws = p.ws; q.total_rows = p.total_rows;
+  q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
+  for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
+  k2_split_expert<TB, CW, RS, K2ParamsCap<CAP>><<<grid, kThreads, k2_smem_bytes(p.d), s>>>(q);
+}
+
+template <int TB, int CW, int RS>
+static void k2_launch_cap(const K2Params& p, int grid, cudaStream_t s) {
+  if (p.nsegs <= 8) k2_launch_t<TB, CW, RS, 8>(p, grid, s);
+  else if (p.nsegs <= 32) k2_launch_t<TB, CW, RS, 32>(p, grid, s);
+  else k2_launch_t<TB, CW, RS, kMaxLaunchSegs>(p, grid, s);
 }
 
 template <int CW, int RS>
 static void k2_dispatch_tb(const K2Params& p, int grid, int tb, cudaStream_t s) {
   switch (tb) {
-    case 1: k2_launch_t<1, CW, RS>(p, grid, s); break;
+    case 1: k2_launch_cap<1, CW, RS>(p, grid, s); break;
     case 2:
-      if constexpr (RS <= 8) k2_launch_t<2, CW, RS>(p, grid, s);
+      if constexpr (RS <= 8) k2_launch_cap<2, CW, RS>(p, grid, s);
       break;
     default:
-      if constexpr (RS <= 4) k2_launch_t<4, CW, RS>(p, grid, s);
+      if constexpr (RS <= 4) k2_launch_cap<4, CW, RS>(p, grid, s);
       break;
   }
 }
@@ -327,8 +351,14 @@ void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s) {
 
 template <int TB, int CW, int RS>
 static cudaError_t k2_attr() {
-  return cudaFuncSetAttribute(k2_split_expert<TB, CW, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              220 * 1024);
+  cudaError_t e = cudaSuccess, r;
+  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, K2ParamsCap<8>>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) != cudaSuccess) e = r;
+  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, K2ParamsCap<32>>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) != cudaSuccess) e = r;
+  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, K2ParamsCap<kMaxLaunchSegs>>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) != cudaSuccess) e = r;
+  return e;
 }
 
 bool kernels_init(char* err, size_t errlen) {

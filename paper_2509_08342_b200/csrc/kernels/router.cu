@@ -114,8 +114,6 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
           float wk = (float)(exp(row[e] - mx) / den);
           p.ids[b * p.K + k] = e;
           p.w[b * p.K + k] = wk;
-          p.mb_ids[b * p.K + k] = e;
-          p.mb_w[b * p.K + k] = wk;
         }
       }
       __syncwarp();
@@ -147,15 +145,24 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
         r += (co > cj) || (co == cj && (mo > mj || (mo == mj && o < j)));
       }
       p.ranking[r] = j;
-      p.mb_rank[r] = j;
     }
   }
+  __syncthreads();
+  // publish to the mapped-pinned mailbox in coalesced bursts (consecutive threads -> consecutive
+  // words, so a warp's writes merge into few PCIe transactions), one system fence, then seq
+  if (p.W0 != nullptr) {
+    for (int i = threadIdx.x; i < p.B * p.K; i += blockDim.x) {
+      p.mb_ids[i] = p.ids[i];
+      p.mb_w[i] = p.w[i];
+    }
+  }
+  if (p.W1 != nullptr)
+    for (int i = threadIdx.x; i < p.N; i += blockDim.x) p.mb_rank[i] = p.ranking[i];
   __syncthreads();
   if (threadIdx.x == 0) {
     *p.ticket = 0u;
     __threadfence_system();
     *p.mb_seq = p.seq;
-    __threadfence_system();
   }
 }
 
