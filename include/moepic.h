@@ -211,7 +211,8 @@ typedef struct {
   double total_ms;
   uint64_t bytes;
 } moepic_kernel_stats;
-enum { MOEPIC_KERNEL_ROUTER = 0, MOEPIC_KERNEL_EXPERT = 1, MOEPIC_KERNEL_COMBINE = 2 };
+enum { MOEPIC_KERNEL_ROUTER = 0, MOEPIC_KERNEL_EXPERT = 1, MOEPIC_KERNEL_COMBINE = 2,
+       MOEPIC_KERNEL_GEMM = 3 /* prefill tcgen05 GEMMs; `bytes` holds algorithmic FLOPs */ };
 /* enable != 0 starts (and resets) event timing; 0 stops it.                                   */
 moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable);
 /* Synchronises the recorded events and returns the totals for one kernel class.               */

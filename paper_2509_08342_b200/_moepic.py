@@ -70,7 +70,7 @@ class moepic_kernel_stats(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("total_ms", C.c_double), ("bytes", C.c_uint64)]
 
 
-KERNEL_ROUTER, KERNEL_EXPERT, KERNEL_COMBINE = 0, 1, 2
+KERNEL_ROUTER, KERNEL_EXPERT, KERNEL_COMBINE, KERNEL_GEMM = 0, 1, 2, 3
 
 _ctxp = C.c_void_p
 _sig = {

@@ -22,9 +22,9 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu"]
+CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu", "kernels/prefill.cu"]
 CXX_SOURCES = ["host/control.cpp", "moepic_api.cpp"]
-HEADERS = ["kernels/kernels.hpp", "kernels/device_utils.cuh", "host/control.hpp", "../../include/moepic.h", "../../include/moepic_hostsim.h"]
+HEADERS = ["kernels/kernels.hpp", "kernels/device_utils.cuh", "kernels/prefill.hpp", "host/control.hpp", "../../include/moepic.h", "../../include/moepic_hostsim.h"]
 
 
 def _newer(target, deps):

@@ -1,0 +1,389 @@
+// Prefill kernels ("experts ... often fully activated"): permute tokens by expert,
+// tcgen05 grouped GEMMs over the split segments, combine.
+//
+// GEMM kernels are warp-specialised, one 128-row output tile per CTA (192 threads):
+//   warp 0  TMA producer: 4-stage ring of 48 KB stages (A 128x64 bf16 + B), 128-byte swizzle,
+//           cp.async.bulk.tensor completing on `full`, waits `empty` before reuse;
+//   warp 1  allocates 256 TMEM columns; one lane issues tcgen05.mma (M = 128, K = 16, fp32
+//           accumulate in TMEM) and tcgen05.commit's each stage back to `empty`, the last one to
+//           `accum`;
+//   warps 2-5 epilogue: tcgen05.ld 32 lanes x 16 columns, SwiGLU (gate/up) or fp32 store (down).
+// gate/up: D_g = X_e W_g^T and D_u = X_e W_u^T share the A tile (two N = 128 MMAs per K step);
+//          a = silu(D_g) * D_u -> bf16 A_act[rows][I] at the segment's intermediate columns.
+// down:    Y[rows][n0..n0+256) (+)= A_act[rows][seg] * Down[seg][n0..], the down rows are
+//          N-contiguous in the row-interleaved layout, so B is an MN-major operand.
+// Weights are read through a 3-D tensor map {d, 3, rows} over the row-interleaved layout
+// [gate_r | up_r | down[:, r]] so the same rows serve both GEMMs without any repacking.
+#include "prefill.hpp"
+#include "kernels.hpp"
+#include "device_utils.cuh"
+
+#include <cstdio>
+#include <cstring>
+
+namespace moepic {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kStageBytes = 48 * 1024;
+constexpr uint32_t kABytes = kPfBM * kPfBK * 2;        // 16 KB
+
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  // K-major, 128-byte swizzle: 8-row groups 1024 B apart (SBO), LBO unused (1), version 1
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // MN-major, 128-byte swizzle: 64-element MN blocks LBO apart, 8-row K groups SBO apart
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn) {
+  // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1), A K-major,
+  // B major bit 16, N >> 3 at bit 17, M >> 4 at bit 24
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  // round-to-nearest-even to bf16
+  const uint32_t ra = (ua + 0x7FFFu + ((ua >> 16) & 1u)) >> 16;
+  const uint32_t rb = (ub + 0x7FFFu + ((ub >> 16) & 1u)) >> 16;
+  return ra | (rb << 16);
+}
+
+template <bool DOWN>
+__global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ PfGemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* accum = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- tile decode
+  int seg = -1, ex = -1, mt = 0, nt = 0;
+  {
+    int t = blockIdx.x;
+    if (!DOWN) {
+      for (int s = 0; s < p.nseg; ++s) {
+        const int ntn = (p.seg[s].nrows + kPfBN1 - 1) / kPfBN1;
+        const int n = p.ex[p.seg[s].e].mtiles * ntn;
+        if (t < n) { seg = s; ex = p.seg[s].e; mt = t / ntn; nt = t - mt * ntn; break; }
+        t -= n;
+      }
+    } else {
+      const int ntn = p.d / kPfBN2;
+      for (int e = 0; e < p.nexp; ++e) {
+        const int n = p.ex[e].mtiles * ntn;
+        if (t < n) { ex = e; mt = t / ntn; nt = t - mt * ntn; break; }
+        t -= n;
+      }
+    }
+  }
+  if (ex < 0) return;
+  const PfExpert E = p.ex[ex];
+  const int arow = E.m_off + mt * kPfBM;      // first row of the A tile / output tile
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // number of K blocks
+  int nkb;
+  if (!DOWN) nkb = p.d / kPfBK;
+  else {
+    nkb = 0;
+    for (int s = E.seg_begin; s < E.seg_end; ++s) nkb += p.seg[s].nrows / kPfBK;
+  }
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int s = DOWN ? E.seg_begin : seg, kin = 0;   // down: current segment and k block inside it
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % kStages;
+        if (kb >= kStages) mbar_wait(&empty[st], ((kb / kStages) - 1) & 1);
+        uint8_t* sa = smem + st * kStageBytes;
+        uint8_t* sb = sa + kABytes;
+        mbar_expect_tx(&full[st], kStageBytes);
+        if (!DOWN) {
+          tma2d(sa, &p.tmA, kb * kPfBK, arow, &full[st]);
+          tma3d(sb, &p.tmB[seg], kb * kPfBK, 0, nt * kPfBN1, &full[st]);
+          tma3d(sb + 16384, &p.tmB[seg], kb * kPfBK, 1, nt * kPfBN1, &full[st]);
+        } else {
+          while (kin >= p.seg[s].nrows / kPfBK) { ++s; kin = 0; }
+          tma2d(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, &full[st]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            tma3d(sb + j * 8192, &p.tmB[s], nt * kPfBN2 + j * 64, 2, kin * kPfBK, &full[st]);
+          ++kin;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = DOWN ? make_idesc(128, kPfBN2, 1) : make_idesc(128, kPfBN1, 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % kStages;
+        mbar_wait(&full[st], (kb / kStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * kStageBytes);
+        const uint32_t sb = sa + kABytes;
+#pragma unroll
+        for (int k = 0; k < kPfBK / 16; ++k) {
+          const uint64_t da = desc_k_sw128(sa + k * 32);
+          const uint32_t acc = (kb | k) ? 1u : 0u;
+          if (!DOWN) {
+            umma(tmem, da, desc_k_sw128(sb + k * 32), idesc, acc);
+            umma(tmem + kPfBN1, da, desc_k_sw128(sb + 16384 + k * 32), idesc, acc);
+          } else {
+            umma(tmem, da, desc_mn_sw128(sb + k * 2048, 8192, 1024), idesc, acc);
+          }
+        }
+        umma_commit(&empty[st]);
+      }
+      umma_commit(accum);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;                       // TMEM lane quarter this warp may access
+    const int m = q * 32 + lane;                  // row within the tile
+    mbar_wait(accum, 0);
+    tc_fence_after();
+    const bool row_ok = mt * kPfBM + m < E.count;
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    if (!DOWN) {
+      const PfSeg S = p.seg[seg];
+      uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + (size_t)(arow + m) * p.ld_out + S.row0 + nt * kPfBN1;
+      for (int c = 0; c < kPfBN1; c += 16) {
+        float g[16], u[16];
+        tmem_ld16(tbase + c, g);
+        tmem_ld16(tbase + kPfBN1 + c, u);
+        if (row_ok && nt * kPfBN1 + c < S.nrows) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
+            const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
+            pk[i] = pack_bf16(a0, a1);
+          }
+          uint4* o = reinterpret_cast<uint4*>(out + c);
+          o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+    } else {
+      float* out = reinterpret_cast<float*>(p.out) + (size_t)(arow + m) * p.ld_out + nt * kPfBN2;
+      for (int c = 0; c < kPfBN2; c += 16) {
+        float v[16];
+        tmem_ld16(tbase + c, v);
+        if (row_ok) {
+          float4* o = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            if (p.accumulate) {
+              const float4 y = o[i];
+              x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+            }
+            o[i] = x;
+          }
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ permute / combine
+__global__ void pf_permute(const __grid_constant__ PfPermuteParams p) {
+  // one warp per (t, k): claim a row of the expert's block, copy h[t] there
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int TK = p.T * p.K;
+  const int total = TK + p.n_shared * p.T;
+  if (gw >= total) return;
+  int row, t;
+  if (gw < TK) {
+    t = gw / p.K;
+    const int e = p.ids[gw];
+    if (e < p.e_lo || e >= p.e_hi) {
+      if (lane == 0) p.pos[gw] = -1;
+      return;
+    }
+    int r = 0;
+    if (lane == 0) r = atomicAdd(&p.cursor[e], 1);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    row = p.m_off[e] + r;
+    if (lane == 0) p.pos[gw] = row;
+  } else {
+    const int s = (gw - TK) / p.T;
+    t = (gw - TK) - s * p.T;
+    row = p.shared_off[s] + t;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(p.h + (size_t)t * p.d);
+  uint4* dst = reinterpret_cast<uint4*>(p.xperm + (size_t)row * p.d);
+  for (int c = lane; c < p.d / 8; c += 32) dst[c] = src[c];
+}
+
+__global__ void pf_combine(const __grid_constant__ PfCombineParams p) {
+  const int t = blockIdx.y;
+  const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c4 * 4 >= p.d) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (p.residual) {
+    const uint2 hv = reinterpret_cast<const uint2*>(p.h + (size_t)t * p.d)[c4];
+    acc = make_float4(bf16lo(hv.x), bf16hi(hv.x), bf16lo(hv.y), bf16hi(hv.y));
+  }
+  for (int k = 0; k < p.K; ++k) {
+    const int r = p.pos[t * p.K + k];
+    if (r < 0) continue;
+    const float w = p.w[t * p.K + k];
+    const float4 v = reinterpret_cast<const float4*>(p.Y + (size_t)r * p.d)[c4];
+    acc.x = fmaf(w, v.x, acc.x); acc.y = fmaf(w, v.y, acc.y);
+    acc.z = fmaf(w, v.z, acc.z); acc.w = fmaf(w, v.w, acc.w);
+  }
+  for (int s = 0; s < p.n_shared; ++s) {
+    const int r = p.shared_off[s] + t;
+    const float4 v = reinterpret_cast<const float4*>(p.Y + (size_t)r * p.d)[c4];
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  reinterpret_cast<float4*>(p.y + (size_t)t * p.d)[c4] = acc;
+}
+
+// ------------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+bool get_encode() {
+  if (g_encode) return true;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return false;
+  g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  return true;
+}
+
+}  // namespace
+
+size_t pf_gemm_smem_bytes() { return kStages * kStageBytes + 1024 + 256; }
+
+bool pf_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  if (!get_encode()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool pf_tmap_weights(CUtensorMap* m, const void* seg_base, uint64_t rows, int d, uint32_t box_rows) {
+  if (!get_encode()) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d, 3, rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)d * 6};
+  cuuint32_t box[3] = {64, 1, box_rows};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(seg_base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_pf_gateup(const PfGemmParams& p, cudaStream_t s) {
+  if (p.ntiles > 0) pf_gemm<false><<<p.ntiles, kThreads, pf_gemm_smem_bytes(), s>>>(p);
+}
+void launch_pf_down(const PfGemmParams& p, cudaStream_t s) {
+  if (p.ntiles > 0) pf_gemm<true><<<p.ntiles, kThreads, pf_gemm_smem_bytes(), s>>>(p);
+}
+void launch_pf_permute(const PfPermuteParams& p, cudaStream_t s) {
+  const int warps = p.T * p.K + p.n_shared * p.T;
+  pf_permute<<<(warps + 7) / 8, 256, 0, s>>>(p);
+}
+void launch_pf_combine(const PfCombineParams& p, cudaStream_t s) {
+  dim3 grid((unsigned)((p.d / 4 + 127) / 128), (unsigned)p.T);
+  pf_combine<<<grid, 128, 0, s>>>(p);
+}
+
+bool prefill_init(char* err, size_t errlen) {
+  cudaError_t e1 = cudaFuncSetAttribute(pf_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)pf_gemm_smem_bytes());
+  cudaError_t e2 = cudaFuncSetAttribute(pf_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)pf_gemm_smem_bytes());
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    snprintf(err, errlen, "prefill attributes: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    return false;
+  }
+  return true;
+}
+
+}  // namespace moepic

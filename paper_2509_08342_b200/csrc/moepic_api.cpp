@@ -25,6 +25,7 @@
 #include "../../include/moepic_hostsim.h"
 #include "host/control.hpp"
 #include "kernels/kernels.hpp"
+#include "kernels/prefill.hpp"
 
 using namespace moepic;
 
@@ -37,7 +38,11 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 struct ArenaLayout {
   size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, total;
   uint64_t pool_rows, plan_rows, od_rows, ws_floats;
+  // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
+  size_t xperm, aact, yperm, pos, cursor;
+  uint64_t pf_rows;
 };
+constexpr int kDecodeMaxB = 32;   // decode path (K2) serves up to 32 tokens (token bit masks)
 
 int n_local(const moepic_model_desc& d) { return d.N / d.ep_size; }
 
@@ -52,7 +57,9 @@ std::string validate_desc(const moepic_model_desc* d) {
   if (d->I < d->row_granule || d->I % d->row_granule != 0) return "I must be a multiple of row_granule";
   if (d->n_shared < 0 || d->n_shared > 8) return "n_shared must be in [0, 8]";
   if (d->buffer_experts < d->K) return "buffer_experts must be >= K";
-  if (d->max_batch < 1 || d->max_batch > 32) return "max_batch must be in [1, 32]";
+  if (d->max_batch < 1 || d->max_batch > 4096) return "max_batch must be in [1, 4096]";
+  if (d->max_batch > kDecodeMaxB && (d->d % 256 != 0 || d->N + d->n_shared > kPfMaxExperts))
+    return "prefill batches (max_batch > 32) need d % 256 == 0 and N + n_shared <= 136";
   if (d->L_host < 1 || d->L_host > d->L) return "L_host must be in [1, L]";
   if (!(d->v_e_max >= 0.0)) return "v_e_max must be >= 0";
   if (d->ep_size < 1 || d->ep_rank < 0 || d->ep_rank >= d->ep_size) return "ep_rank / ep_size invalid";
@@ -72,13 +79,25 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   a.plan_rows = (uint64_t)d.buffer_experts * d.I;
   a.od_rows = (uint64_t)std::min(Nl, d.max_batch * d.K) * d.I;
   for (int i = 0; i < 2; ++i) { a.buf[i] = off; off = align_up(off + (a.plan_rows + a.od_rows) * rb); }
-  a.ws_floats = (uint64_t)d.d * (4ull * (d.max_batch * d.K + d.n_shared * d.max_batch) + 3ull * (kSMs + 1) * 8 + 64);
+  const uint64_t Bd = (uint64_t)std::min(d.max_batch, kDecodeMaxB);
+  a.ws_floats = (uint64_t)d.d * (4ull * (Bd * d.K + d.n_shared * Bd) + 3ull * (kSMs + 1) * 8 + 64);
   a.ws = off; off = align_up(off + a.ws_floats * 4);
   a.logits = off; off = align_up(off + (size_t)2 * d.max_batch * d.N * 8);
   a.ids = off; off = align_up(off + (size_t)d.max_batch * d.K * 4);
   a.w = off; off = align_up(off + (size_t)d.max_batch * d.K * 4);
   a.ranking = off; off = align_up(off + (size_t)d.N * 4);
   a.ticket = off; off = align_up(off + 64);
+  a.pf_rows = 0;
+  a.xperm = a.aact = a.yperm = a.pos = a.cursor = off;
+  if (d.max_batch > kDecodeMaxB) {
+    const uint64_t T = d.max_batch;
+    a.pf_rows = T * d.K + (uint64_t)d.N * (kPfBM - 1) + (uint64_t)d.n_shared * (T + kPfBM - 1) + kPfBM;
+    a.xperm = off; off = align_up(off + a.pf_rows * d.d * 2, 1024);
+    a.aact = off; off = align_up(off + a.pf_rows * d.I * 2, 1024);
+    a.yperm = off; off = align_up(off + a.pf_rows * d.d * 4);
+    a.pos = off; off = align_up(off + T * d.K * 4);
+    a.cursor = off; off = align_up(off + (size_t)d.N * 4);
+  }
   a.total = off;
   return a;
 }
@@ -244,7 +263,7 @@ struct moepic_ctx {
   bool profiling = false;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
-  moepic_kernel_stats prof_acc[3]{};
+  moepic_kernel_stats prof_acc[4]{};
 
   int prof_begin(cudaStream_t s, int cls) {
     if (!profiling) return -1;
@@ -351,6 +370,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
     return st;
   };
   if (!kernels_init(kerr, sizeof kerr)) return bail(MOEPIC_ERUNTIME);
+  if (desc->max_batch > kDecodeMaxB && !prefill_init(kerr, sizeof kerr)) return bail(MOEPIC_ERUNTIME);
   const uint64_t host_bytes = (uint64_t)desc->L_host * ctx->Nl() * desc->I * ctx->rb();
   if (cudaHostAlloc(&ctx->host_experts, host_bytes, cudaHostAllocDefault) != cudaSuccess) {
     cudaGetLastError();
@@ -469,7 +489,8 @@ moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg, 
 struct StepSeg {
   const uint8_t* base;
   int32_t expert, nrows;
-  uint32_t mask;
+  uint32_t mask;    // decode: tokens served (bit b = token b)
+  int32_t row0;     // first intermediate index of the segment inside its expert
 };
 
 static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& segs, const uint16_t* h, int B,
@@ -664,6 +685,158 @@ static moepic_status finish_plan(moepic_ctx* ctx, const Plan& plan, const StepRe
   return MOEPIC_OK;
 }
 
+// Prefill batch (B > 32): tokens are permuted into per-expert blocks (padded to 128 rows), every
+// segment group runs the tcgen05 gate/up GEMM (SwiGLU epilogue into A_act) and the down GEMM
+// (accumulating into Y), then each token gathers its K rows.  Groups: resident tops + shared
+// experts first (no wait), then prefetched segments (plan event), then on-demand ones (copy
+// event), so the resident work overlaps the PCIe loads.
+static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, float* y, cudaStream_t s,
+                                    uint32_t flags, const std::vector<StepSeg>& gA,
+                                    const std::vector<StepSeg>& gB, const std::vector<StepSeg>& gC, int buf,
+                                    int& launches) {
+  const auto& d = ctx->desc;
+  const int N = d.N, K = d.K, NS = d.n_shared, NE = N + NS;
+  const int lo_e = d.ep_rank * ctx->Nl(), hi_e = lo_e + ctx->Nl();
+  std::vector<int32_t> cnt(NE, 0), moff(NE, 0);
+  for (int i = 0; i < T * K; ++i) {
+    const int e = ctx->ids_h[i];
+    if (e >= lo_e && e < hi_e) cnt[e]++;
+  }
+  for (int s2 = 0; s2 < NS; ++s2) cnt[N + s2] = T;
+  int64_t rows = 0;
+  std::vector<PfExpert> table(NE);
+  for (int e = 0; e < NE; ++e) {
+    moff[e] = (int32_t)rows;
+    const int mt = (cnt[e] + kPfBM - 1) / kPfBM;
+    table[e] = PfExpert{(int32_t)rows, cnt[e], mt, 0, 0, {0, 0, 0}};
+    rows += (int64_t)mt * kPfBM;
+  }
+  if ((uint64_t)rows + kPfBM > ctx->lay.pf_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "prefill row overflow");
+  uint16_t* xperm = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.xperm);
+  uint16_t* aact = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.aact);
+  float* Y = reinterpret_cast<float*>(ctx->arena + ctx->lay.yperm);
+  int32_t* pos = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.pos);
+  int32_t* cursor = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.cursor);
+
+  // ---- permute (+ zero the accumulated outputs)
+  CK(cudaMemsetAsync(cursor, 0, (size_t)N * 4, s));
+  CK(cudaMemsetAsync(Y, 0, (size_t)rows * d.d * 4, s));
+  static PfPermuteParams pp;
+  pp.h = h; pp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids); pp.cursor = cursor;
+  pp.pos = pos; pp.xperm = xperm; pp.T = T; pp.K = K; pp.d = d.d; pp.e_lo = lo_e; pp.e_hi = hi_e;
+  pp.n_shared = NS;
+  for (int s2 = 0; s2 < NS; ++s2) pp.shared_off[s2] = moff[N + s2];
+  for (int e = 0; e < N; ++e) pp.m_off[e] = moff[e];
+  launch_pf_permute(pp, s);
+  CK(cudaGetLastError());
+  ++launches;
+
+  static PfGemmParams gp;
+  CUtensorMap tm_x, tm_act;
+  if (!pf_tmap_2d(&tm_x, xperm, (uint64_t)rows + kPfBM, d.d, kPfBM) ||
+      !pf_tmap_2d(&tm_act, aact, (uint64_t)rows + kPfBM, d.I, kPfBM))
+    return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (activations)");
+  auto tidx = [&](int expert) { return expert >= 0 ? expert : N + (-1 - expert); };
+
+  auto run_group = [&](const std::vector<StepSeg>& g) -> moepic_status {
+    for (const auto& sg : g)
+      if (sg.nrows % kPfBK != 0 || (reinterpret_cast<uintptr_t>(sg.base) & 15))
+        return fail(&ctx->err, MOEPIC_ERUNTIME, "prefill segment rows must be a multiple of 64");
+    // gate/up: chunks of <= kPfMaxSegs segments
+    for (size_t i0 = 0; i0 < g.size(); i0 += kPfMaxSegs) {
+      const size_t i1 = std::min(g.size(), i0 + (size_t)kPfMaxSegs);
+      gp.tmA = tm_x;
+      gp.nseg = (int)(i1 - i0);
+      gp.nexp = NE;
+      for (int e = 0; e < NE; ++e) gp.ex[e] = table[e];
+      int64_t tiles = 0;
+      double flops = 0;
+      for (size_t i = i0; i < i1; ++i) {
+        const StepSeg& sg = g[i];
+        const int e = tidx(sg.expert);
+        gp.seg[i - i0] = PfSeg{e, sg.row0, sg.nrows, 0};
+        if (!pf_tmap_weights(&gp.tmB[i - i0], sg.base, (uint64_t)sg.nrows, d.d, kPfBN1))
+          return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (weights)");
+        tiles += (int64_t)table[e].mtiles * ((sg.nrows + kPfBN1 - 1) / kPfBN1);
+        flops += 2.0 * 2.0 * cnt[e] * (double)d.d * sg.nrows;
+      }
+      gp.ntiles = (int32_t)tiles;
+      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.ld_out = d.I; gp.accumulate = 0;
+      const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
+      launch_pf_gateup(gp, s);
+      ctx->prof_end(pe, s, (uint64_t)flops);
+      CK(cudaGetLastError());
+      ++launches;
+    }
+    // down: experts' segments are consecutive in g; chunk by whole experts
+    size_t i0 = 0;
+    while (i0 < g.size()) {
+      size_t i1 = i0;
+      while (i1 < g.size()) {
+        size_t j = i1;
+        while (j < g.size() && g[j].expert == g[i1].expert) ++j;
+        if (j - i0 > (size_t)kPfMaxSegs && i1 > i0) break;
+        i1 = j;
+      }
+      gp.tmA = tm_act;
+      gp.nseg = (int)(i1 - i0);
+      gp.nexp = NE;
+      for (int e = 0; e < NE; ++e) {
+        gp.ex[e] = table[e];
+        gp.ex[e].mtiles = 0;
+      }
+      double flops = 0;
+      for (size_t i = i0; i < i1; ++i) {
+        const StepSeg& sg = g[i];
+        const int e = tidx(sg.expert);
+        const int li = (int)(i - i0);
+        gp.seg[li] = PfSeg{e, sg.row0, sg.nrows, 0};
+        if (!pf_tmap_weights(&gp.tmB[li], sg.base, (uint64_t)sg.nrows, d.d, kPfBK))
+          return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (weights)");
+        if (gp.ex[e].mtiles == 0) {
+          gp.ex[e].mtiles = table[e].mtiles;
+          gp.ex[e].seg_begin = li;
+        }
+        gp.ex[e].seg_end = li + 1;
+        flops += 2.0 * cnt[e] * (double)d.d * sg.nrows;
+      }
+      int64_t tiles = 0;
+      for (int e = 0; e < NE; ++e) tiles += (int64_t)gp.ex[e].mtiles * (d.d / kPfBN2);
+      gp.ntiles = (int32_t)tiles;
+      gp.d = d.d; gp.I = d.I; gp.out = Y; gp.ld_out = d.d; gp.accumulate = 1;
+      const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
+      launch_pf_down(gp, s);
+      ctx->prof_end(pe, s, (uint64_t)flops);
+      CK(cudaGetLastError());
+      ++launches;
+      i0 = i1;
+    }
+    return MOEPIC_OK;
+  };
+  moepic_status st = run_group(gA);
+  if (st != MOEPIC_OK) return st;
+  if (!gB.empty()) {
+    CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
+    if ((st = run_group(gB)) != MOEPIC_OK) return st;
+  }
+  if (!gC.empty()) {
+    CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
+    if ((st = run_group(gC)) != MOEPIC_OK) return st;
+  }
+  PfCombineParams cp2{};
+  cp2.y = y; cp2.h = h; cp2.Y = Y; cp2.pos = pos;
+  cp2.w = reinterpret_cast<const float*>(ctx->arena + ctx->lay.w);
+  cp2.T = T; cp2.K = K; cp2.d = d.d; cp2.n_shared = NS;
+  cp2.residual = ((flags & MOEPIC_RESIDUAL) && d.ep_rank == 0) ? 1 : 0;
+  for (int s2 = 0; s2 < NS; ++s2) cp2.shared_off[s2] = moff[N + s2];
+  const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_COMBINE);
+  launch_pf_combine(cp2, s);
+  ctx->prof_end(pe, s, (uint64_t)T * K * d.d * 4 + (uint64_t)T * d.d * 4);
+  CK(cudaGetLastError());
+  ++launches;
+  return MOEPIC_OK;
+}
+
 moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B, float* y_dev,
                                    void* stream, uint32_t flags, moepic_trace* tr) {
   CTX_GUARD();
@@ -707,6 +880,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   const int K = d.K;
   auto mask_of = [&](int e) {
     uint32_t m = 0;
+    if (B > kDecodeMaxB) return m;      // prefill segments carry no token masks
     for (int b = 0; b < B; ++b)
       for (int k = 0; k < K; ++k)
         if (ctx->ids_h[b * K + k] == e) m |= 1u << b;
@@ -725,7 +899,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   {
     const int64_t lo = shared_lo(cp), hi = shared_hi(cp);
     for (int s2 = 0; s2 < d.n_shared; ++s2)
-      if (hi > lo) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2) + lo * rb, -1 - s2, (int32_t)(hi - lo), all_tok});
+      if (hi > lo) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2) + lo * rb, -1 - s2, (int32_t)(hi - lo), all_tok, (int32_t)lo});
   }
   for (size_t a = 0; a < res.A.size(); ++a) {
     const int e = res.A[a];
@@ -735,11 +909,11 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     const uint8_t* hsrc = ctx->host_expert(layer, e);
     const bool top_cached_before = (c != kGamma) && !(pj >= 0 && used.items[pj].full);
     if (top_cached_before && l.I_top > 0) {
-      gA.push_back(StepSeg{ctx->slot_ptr(layer, l.slot_of[e]), e, l.I_top, m});
+      gA.push_back(StepSeg{ctx->slot_ptr(layer, l.slot_of[e]), e, l.I_top, m, 0});
     }
     if (pj >= 0) {
       const PlanItem& it = used.items[pj];
-      gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m});
+      gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m, it.full ? 0 : l.I_top});
       continue;   // alpha: nothing missing
     }
     if (c == kBeta) {
@@ -747,7 +921,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       uint8_t* dst = ctx->od_ptr(buf, od_row);
       CK(cudaMemcpyAsync(dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows * rb, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies++;
-      gC.push_back(StepSeg{dst, e, rows, m});
+      gC.push_back(StepSeg{dst, e, rows, m, l.I_top});
       od_row += rows;
       any_od = true;
     } else if (c == kGamma) {
@@ -756,21 +930,21 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
         uint8_t* top = ctx->slot_ptr(layer, slot);
         CK(cudaMemcpyAsync(top, hsrc, (size_t)l.I_top * rb, cudaMemcpyHostToDevice, ctx->copy));
         ctx->ctr.h2d_copies++;
-        gC.push_back(StepSeg{top, e, l.I_top, m});
+        gC.push_back(StepSeg{top, e, l.I_top, m, 0});
         const int rows = d.I - l.I_top;
         if (rows > 0) {
           uint8_t* dst = ctx->od_ptr(buf, od_row);
           CK(cudaMemcpyAsync(dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows * rb, cudaMemcpyHostToDevice,
                              ctx->copy));
           ctx->ctr.h2d_copies++;
-          gC.push_back(StepSeg{dst, e, rows, m});
+          gC.push_back(StepSeg{dst, e, rows, m, l.I_top});
           od_row += rows;
         }
       } else {
         uint8_t* dst = ctx->od_ptr(buf, od_row);
         CK(cudaMemcpyAsync(dst, hsrc, (size_t)d.I * rb, cudaMemcpyHostToDevice, ctx->copy));
         ctx->ctr.h2d_copies++;
-        gC.push_back(StepSeg{dst, e, d.I, m});
+        gC.push_back(StepSeg{dst, e, d.I, m, 0});
         od_row += d.I;
       }
       any_od = true;
@@ -779,6 +953,11 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   if ((uint64_t)od_row > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
   if (any_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
 
+  if (B > kDecodeMaxB) {
+    // ---- prefill: permute, tcgen05 GEMMs per segment group, combine
+    st = prefill_launch(ctx, h, B, y_dev, s, flags, gA, gB, gC, buf, launches);
+    if (st != MOEPIC_OK) return st;
+  } else {
   // ---- K2 launches: resident now / prefetched / on-demand, then the combine
   int64_t ws_next = 0;
   std::vector<CombineSeg> comb;
@@ -813,6 +992,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   }
   CK(cudaGetLastError());
   ++launches;
+  }
   // alpha experts that arrived as full prefetches and were admitted: D2D their top rows
   for (const auto& a : res.adm) {
     if (!a.d2d_from_plan || a.victim == kAdmNone || l.I_top == 0) continue;
@@ -995,7 +1175,7 @@ moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable) {
 
 moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_kernel_stats* out) {
   CTX_GUARD();
-  if (!out || kernel_class < 0 || kernel_class > 2) return fail(&ctx->err, MOEPIC_EINVAL, "bad profile_read args");
+  if (!out || kernel_class < 0 || kernel_class > 3) return fail(&ctx->err, MOEPIC_EINVAL, "bad profile_read args");
   ctx->prof_drain();
   *out = ctx->prof_acc[kernel_class];
   return MOEPIC_OK;
