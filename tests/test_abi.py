@@ -42,7 +42,7 @@ def test_arena_bytes_and_desc_validation():
     assert M.moepic_arena_bytes(ctypes.byref(d), ctypes.byref(n)) == M.OK
     # slot pool of 128 experts (45 GB) + 2 ping-pong halves of 4 experts
     assert n.value > 128 * 352321536 + 2 * 4 * 352321536
-    for bad in (dict(K=8), dict(d=4100), dict(I=1000), dict(max_batch=64), dict(L_host=40)):
+    for bad in (dict(K=8), dict(d=4100), dict(I=1000), dict(max_batch=8192), dict(L_host=40)):
         kw = dict(L=32, N=8, K=2, d=4096, I=14336, max_batch=1, v_e_max=128, L_host=2)
         kw.update(bad)
         d = api.model_desc(**kw)
