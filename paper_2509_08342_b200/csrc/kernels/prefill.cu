@@ -25,11 +25,15 @@ namespace moepic {
 
 namespace {
 
-constexpr int kStages = 4;
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kStageBytes = 48 * 1024;
 constexpr uint32_t kABytes = kPfBM * kPfBK * 2;        // 16 KB
+// gate/up stage: A | B_gate | B_up (48 KB) x 4;  down stage: A_hi | A_lo | B (64 KB) x 3
+template <bool DOWN> struct Cfg {
+  static constexpr int kStages = DOWN ? 3 : 4;
+  static constexpr uint32_t kStageBytes = DOWN ? 64 * 1024 : 48 * 1024;
+  static constexpr uint32_t kBOff = DOWN ? 2 * kABytes : kABytes;
+};
 
 __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   // K-major, 128-byte swizzle: 8-row groups 1024 B apart (SBO), LBO unused (1), version 1
@@ -87,16 +91,22 @@ __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, i
       : "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
-  // round-to-nearest-even to bf16
-  const uint32_t ra = (ua + 0x7FFFu + ((ua >> 16) & 1u)) >> 16;
-  const uint32_t rb = (ub + 0x7FFFu + ((ub >> 16) & 1u)) >> 16;
-  return ra | (rb << 16);
+__device__ __forceinline__ uint32_t bf16_rne(float a) {   // round-to-nearest-even to bf16 bits
+  const uint32_t u = __float_as_uint(a);
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+// a = hi + lo with hi = bf16(a), lo = bf16(a - hi): the down GEMM consumes both (2 MMAs), so the
+// intermediate activation carries ~16 mantissa bits instead of bf16's 8
+__device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) {
+  hi = bf16_rne(a);
+  lo = bf16_rne(a - __uint_as_float(hi << 16));
 }
 
 template <bool DOWN>
 __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ PfGemmParams p) {
+  constexpr int kStages = Cfg<DOWN>::kStages;
+  constexpr uint32_t kStageBytes = Cfg<DOWN>::kStageBytes;
+  constexpr uint32_t kBOff = Cfg<DOWN>::kBOff;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
         const int st = kb % kStages;
         if (kb >= kStages) mbar_wait(&empty[st], ((kb / kStages) - 1) & 1);
         uint8_t* sa = smem + st * kStageBytes;
-        uint8_t* sb = sa + kABytes;
+        uint8_t* sb = sa + kBOff;
         mbar_expect_tx(&full[st], kStageBytes);
         if (!DOWN) {
           tma2d(sa, &p.tmA, kb * kPfBK, arow, &full[st]);
@@ -172,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
         } else {
           while (kin >= p.seg[s].nrows / kPfBK) { ++s; kin = 0; }
           tma2d(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, &full[st]);
+          tma2d(sa + kABytes, &p.tmA2, p.seg[s].row0 + kin * kPfBK, arow, &full[st]);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             tma3d(sb + j * 8192, &p.tmB[s], nt * kPfBN2 + j * 64, 2, kin * kPfBK, &full[st]);
@@ -188,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
         mbar_wait(&full[st], (kb / kStages) & 1);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + st * kStageBytes);
-        const uint32_t sb = sa + kABytes;
+        const uint32_t sb = sa + kBOff;
 #pragma unroll
         for (int k = 0; k < kPfBK / 16; ++k) {
           const uint64_t da = desc_k_sw128(sa + k * 32);
@@ -197,7 +208,9 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
             umma(tmem, da, desc_k_sw128(sb + k * 32), idesc, acc);
             umma(tmem + kPfBN1, da, desc_k_sw128(sb + 16384 + k * 32), idesc, acc);
           } else {
-            umma(tmem, da, desc_mn_sw128(sb + k * 2048, 8192, 1024), idesc, acc);
+            const uint64_t db = desc_mn_sw128(sb + k * 2048, 8192, 1024);
+            umma(tmem, da, db, idesc, acc);
+            umma(tmem, desc_k_sw128(sa + kABytes + k * 32), db, idesc, 1u);   // + A_lo * B
           }
         }
         umma_commit(&empty[st]);
@@ -214,22 +227,31 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
     if (!DOWN) {
       const PfSeg S = p.seg[seg];
-      uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + (size_t)(arow + m) * p.ld_out + S.row0 + nt * kPfBN1;
+      const size_t off = (size_t)(arow + m) * p.ld_out + S.row0 + nt * kPfBN1;
+      uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + off;
+      uint16_t* out_lo = reinterpret_cast<uint16_t*>(p.out2) + off;
       for (int c = 0; c < kPfBN1; c += 16) {
         float g[16], u[16];
         tmem_ld16(tbase + c, g);
         tmem_ld16(tbase + kPfBN1 + c, u);
         if (row_ok && nt * kPfBN1 + c < S.nrows) {
-          uint32_t pk[8];
+          uint32_t ph[8], pl[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
             const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
-            pk[i] = pack_bf16(a0, a1);
+            uint32_t h0, l0, h1, l1;
+            split_bf16(a0, h0, l0);
+            split_bf16(a1, h1, l1);
+            ph[i] = h0 | (h1 << 16);
+            pl[i] = l0 | (l1 << 16);
           }
           uint4* o = reinterpret_cast<uint4*>(out + c);
-          o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          o[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+          o[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
+          uint4* ol = reinterpret_cast<uint4*>(out_lo + c);
+          ol[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+          ol[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
         }
       }
     } else {
@@ -335,7 +357,7 @@ bool get_encode() {
 
 }  // namespace
 
-size_t pf_gemm_smem_bytes() { return kStages * kStageBytes + 1024 + 256; }
+size_t pf_gemm_smem_bytes() { return 3 * 64 * 1024 + 1024 + 256; }   // max of both configs (192 KB)
 
 bool pf_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   if (!get_encode()) return false;

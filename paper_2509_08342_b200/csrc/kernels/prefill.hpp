@@ -33,14 +33,16 @@ struct PfExpert {
 };
 
 struct PfGemmParams {
-  CUtensorMap tmA;                    // A operand: X_perm (gate/up) or A_act (down), 2-D
+  CUtensorMap tmA;                    // A operand: X_perm (gate/up) or A_act hi (down), 2-D
+  CUtensorMap tmA2;                   // down: A_act lo (a = hi + lo)
   CUtensorMap tmB[kPfMaxSegs];        // weight segments, 3-D {d, 3, rows}
   PfSeg seg[kPfMaxSegs];
   PfExpert ex[kPfMaxExperts];
   int32_t nseg, nexp;
   int32_t ntiles;                     // total output tiles of the launch
   int32_t d, I;
-  void* out;                          // gate/up: bf16 A_act [rows][I]; down: fp32 Y [rows][d]
+  void* out;                          // gate/up: bf16 A_act hi [rows][I]; down: fp32 Y [rows][d]
+  void* out2;                         // gate/up: bf16 A_act lo [rows][I]
   int32_t ld_out;                     // elements per output row
   int32_t accumulate;                 // down: add into `out` (second segment group)
 };

@@ -93,7 +93,7 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
     const uint64_t T = d.max_batch;
     a.pf_rows = T * d.K + (uint64_t)d.N * (kPfBM - 1) + (uint64_t)d.n_shared * (T + kPfBM - 1) + kPfBM;
     a.xperm = off; off = align_up(off + a.pf_rows * d.d * 2, 1024);
-    a.aact = off; off = align_up(off + a.pf_rows * d.I * 2, 1024);
+    a.aact = off; off = align_up(off + a.pf_rows * d.I * 4, 1024);
     a.yperm = off; off = align_up(off + a.pf_rows * d.d * 4);
     a.pos = off; off = align_up(off + T * d.K * 4);
     a.cursor = off; off = align_up(off + (size_t)d.N * 4);
@@ -714,6 +714,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   if ((uint64_t)rows + kPfBM > ctx->lay.pf_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "prefill row overflow");
   uint16_t* xperm = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.xperm);
   uint16_t* aact = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.aact);
+  uint16_t* aact_lo = aact + ctx->lay.pf_rows * d.I;   // a = hi + lo
   float* Y = reinterpret_cast<float*>(ctx->arena + ctx->lay.yperm);
   int32_t* pos = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.pos);
   int32_t* cursor = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.cursor);
@@ -732,9 +733,10 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   ++launches;
 
   static PfGemmParams gp;
-  CUtensorMap tm_x, tm_act;
+  CUtensorMap tm_x, tm_act, tm_act_lo;
   if (!pf_tmap_2d(&tm_x, xperm, (uint64_t)rows + kPfBM, d.d, kPfBM) ||
-      !pf_tmap_2d(&tm_act, aact, (uint64_t)rows + kPfBM, d.I, kPfBM))
+      !pf_tmap_2d(&tm_act, aact, (uint64_t)rows + kPfBM, d.I, kPfBM) ||
+      !pf_tmap_2d(&tm_act_lo, aact_lo, (uint64_t)rows + kPfBM, d.I, kPfBM))
     return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (activations)");
   auto tidx = [&](int expert) { return expert >= 0 ? expert : N + (-1 - expert); };
 
@@ -761,7 +763,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         flops += 2.0 * 2.0 * cnt[e] * (double)d.d * sg.nrows;
       }
       gp.ntiles = (int32_t)tiles;
-      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.ld_out = d.I; gp.accumulate = 0;
+      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.out2 = aact_lo; gp.ld_out = d.I; gp.accumulate = 0;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
       launch_pf_gateup(gp, s);
       ctx->prof_end(pe, s, (uint64_t)flops);
@@ -779,6 +781,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         i1 = j;
       }
       gp.tmA = tm_act;
+      gp.tmA2 = tm_act_lo;
       gp.nseg = (int)(i1 - i0);
       gp.nexp = NE;
       for (int e = 0; e < NE; ++e) {

@@ -89,7 +89,7 @@ def _unit_u(seed: int, d: int) -> torch.Tensor:
     return u / u.norm()
 
 
-def router_weights(seed: int, layer: int, N: int, d: int, kappa: float = 1.0) -> torch.Tensor:
+def router_weights(seed: int, layer: int, N: int, d: int, kappa: float = 0.5) -> torch.Tensor:
     """Router R^i as bf16 [N][d] with a Zipf-like popularity bias along u."""
     g = _gen(seed, 3, layer)
     base = torch.randn(N, d, generator=g, dtype=torch.float64) / math.sqrt(d)
@@ -101,7 +101,7 @@ def router_weights(seed: int, layer: int, N: int, d: int, kappa: float = 1.0) ->
     return w.to(torch.bfloat16)
 
 
-def hidden_states(seed: int, T: int, L: int, d: int, mu: float = 1.0, a: float = 0.8,
+def hidden_states(seed: int, T: int, L: int, d: int, mu: float = 1.0, a: float = 0.35,
                   eps: float = 0.35, scale: float = 1.0) -> torch.Tensor:
     """h[t][i] bf16 [T][L][d]: AR(1) token process + per-layer perturbation."""
     g = _gen(seed, 4, T, L)
