@@ -34,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MoE-layer decode throughput at 50% expert VRAM budget (tokens/s through the MoE stack)"
+METRIC_PREFILL = "MoE-layer prefill throughput at 50% expert VRAM budget (tokens/s through the MoE stack)"
 
 CONFIGS = {
     # name: (shape, L, L_host, B, v_e fraction, theta)
@@ -41,6 +42,8 @@ CONFIGS = {
     "qwen3": dict(shape="qwen3", L=48, L_host=4, B=1, budget=0.5, theta=0.5, adaptive=True),
     "deepseek": dict(shape="deepseek", L=26, L_host=4, B=1, budget=0.5, theta=0.5),
     "toy": dict(shape="toy", L=2, L_host=2, B=1, budget=0.25, theta=0.5),
+    # BJ configs[4]: Mixtral-shaped prefill of 2048 tokens through a 4-layer stack (tcgen05 GEMMs)
+    "mixtral_prefill": dict(shape="mixtral", L=4, L_host=2, B=2048, budget=0.5, theta=0.5, prefill=True),
 }
 
 
@@ -241,6 +244,7 @@ def run_ours(args, log):
     k2 = ctx.profile_read(api.M.KERNEL_EXPERT)
     k1 = ctx.profile_read(api.M.KERNEL_ROUTER)
     k3 = ctx.profile_read(api.M.KERNEL_COMBINE)
+    kg = ctx.profile_read(api.M.KERNEL_GEMM)
     ctx.profile(False)
     dc = {k: c1[k] - c0[k] for k in c1}
     tokens = args.steps * B
@@ -266,15 +270,33 @@ def run_ours(args, log):
 
     peaks = _peaks()
     hbm_peak = float(peaks["hbm_gbs"])
+    hbm_peak_note = "MEASURED_PEAKS.json"
     k2_gbs = k2["bytes"] / (k2["total_ms"] * 1e-3) / 1e9 if k2["total_ms"] > 0 else 0.0
     pcie_moved = dc["pcie_ondemand_bytes"] + dc["pcie_prefetch_bytes"]
     t_roof = max(dc["hbm_bytes"] / (hbm_peak * 1e9), pcie_moved / (pcie * 1e9))
+    prefill = bool(cfg.get("prefill"))
+    if prefill:
+        tf = kg["bytes"] / (kg["total_ms"] * 1e-3) / 1e12 if kg["total_ms"] > 0 else 0.0
+        tpeak = float(peaks.get("bf16_tflops_sustained", 1440.6))
+        roof = {"bound": "tensor", "kernel": "pf_gemm (tcgen05 gate/up + down)", "achieved": round(tf, 1),
+                "peak": tpeak, "unit": "TFLOP/s", "frac": round(tf / tpeak, 4), "traffic": None,
+                "launches": kg["launches"], "avg_launch_us": round(kg["total_ms"] * 1e3 / max(1, kg["launches"]), 2),
+                "flops_per_launch": int(kg["bytes"] / max(1, kg["launches"])),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
+    else:
+        roof = {"bound": "hbm", "kernel": "k2_split_expert", "achieved": round(k2_gbs, 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(k2_gbs / hbm_peak, 4), "traffic": None,
+                "launches": k2["launches"], "avg_launch_us": round(k2["total_ms"] * 1e3 / max(1, k2["launches"]), 2),
+                "bytes_per_launch": int(k2["bytes"] / max(1, k2["launches"])),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"}
     out = {
-        "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
+        "metric": METRIC_PREFILL if prefill else METRIC, "value": round(value, 4), "unit": "tokens/s",
+        "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded random weights, organic routing process; synth/)",
-        "config": {"workload": f"{args.config}-shaped decode, B={B}, {cfg['budget']:.0%} expert VRAM budget",
+        "config": {"workload": f"{cfg['shape']}-shaped {'prefill' if prefill else 'decode'}, B={B}, "
+                               f"{cfg['budget']:.0%} expert VRAM budget",
                    "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
                    "global_batch": B, "seq_len": 1, "parallelism": f"ep{world}" if world > 1 else "single",
                    "v_e_experts": v_e, "theta": cfg["theta"], "policy": "LCP", "y_cap": S.K * B,
@@ -286,11 +308,7 @@ def run_ours(args, log):
                              "p50_token_ms": round(statistics.median(tok_ms), 3),
                              "p95_token_ms": round(sorted(tok_ms)[max(0, math.ceil(0.95 * len(tok_ms)) - 1)], 3)},
         "gpu_launches": int(dc["kernel_launches"]),
-        "roofline": {"bound": "hbm", "kernel": "k2_split_expert", "achieved": round(k2_gbs, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(k2_gbs / hbm_peak, 4), "traffic": None,
-                     "launches": k2["launches"], "avg_launch_us": round(k2["total_ms"] * 1e3 / max(1, k2["launches"]), 2),
-                     "bytes_per_launch": int(k2["bytes"] / max(1, k2["launches"])),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
+        "roofline": roof,
         "path_roofline": {"bound": "pcie" if pcie_moved / pcie > dc["hbm_bytes"] / hbm_peak else "hbm",
                           "pcie_peak_gbs": round(pcie, 2), "pcie_nominal_gbs": 63.0,
                           "pcie_bytes_moved": pcie_moved, "pcie_ondemand_bytes": dc["pcie_ondemand_bytes"],
@@ -299,6 +317,7 @@ def run_ours(args, log):
                           "frac": round(t_roof * 1e3 / ms, 4),
                           "achieved_pcie_gbs": round(pcie_moved / (ms * 1e-3) / 1e9, 2)},
         "kernels_ms": {"router": round(k1["total_ms"], 3), "expert": round(k2["total_ms"], 3),
+                       "gemm": round(kg["total_ms"], 3),
                        "combine": round(k3["total_ms"], 3)},
         "cache": {"alpha": dc["act_alpha"], "beta": dc["act_beta"], "gamma": dc["act_gamma"],
                   "pred_hit_rate": round(dc["pred_hits"] / max(1, dc["pred_total"]), 4)},
@@ -328,19 +347,20 @@ def cpu_baseline(keep, S, cfg, args, log, n_layer_steps=3):
     except Exception:
         cores = os.cpu_count()
     router = synth.bf16_bits(synth.router_weights(0, 0, S.N, S.d))
-    H = synth.hidden_states(1, n_layer_steps, 1, S.d)
+    nt = min(cfg["B"], 64)                     # tokens per sampled layer step (prefill: 64 of 2048)
+    H = synth.hidden_states(1, n_layer_steps * nt, 1, S.d)
     missing = [e for e in range(S.N) if e not in keep]
     if missing:
         return None
     ts = []
     for t in range(n_layer_steps):
-        hb = synth.bf16_bits(H[t, 0][None])
+        hb = synth.bf16_bits(H[t * nt:(t + 1) * nt, 0])
         t0 = time.perf_counter()
         _oracle_layer_step(S, cfg, keep, hb, router)
         ts.append(time.perf_counter() - t0)
     per_layer = statistics.mean(ts)
-    return {"value": round(1.0 / (per_layer * cfg["L"]), 6), "unit": "tokens/s", "cores": cores,
-            "kind": "oracle", "sample": f"{n_layer_steps} single-token layer steps of layer 0 (fp64 numpy), "
+    return {"value": round(nt / (per_layer * cfg["L"]), 6), "unit": "tokens/s", "cores": cores,
+            "kind": "oracle", "sample": f"{n_layer_steps} layer steps of {nt} token(s), layer 0 (fp64 numpy), "
                                         f"{per_layer * 1e3:.0f} ms each, extrapolated x{cfg['L']} layers",
             "cpu": _cpu_name()}
 
