@@ -20,7 +20,7 @@ import synth  # noqa: E402
 from paper_2509_08342_b200 import api  # noqa: E402
 
 
-def run(shape, B, steps, L=2, theta=1.0):
+def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
     S = synth.SHAPES[shape]
     desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=64, max_batch=B,
                           renorm_topk=S.renorm, L_host=1, v_e_max=L * S.N)
@@ -44,6 +44,13 @@ def run(shape, B, steps, L=2, theta=1.0):
         for i in range(L):
             ctx.layer_forward(i, hsel(t, i), y, stream=st, trace=False)
     torch.cuda.synchronize()
+    if pcie_load:   # saturate the H2D link with a background copy loop on another stream
+        hsrc = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        hdst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        bg = torch.cuda.Stream()
+        with torch.cuda.stream(bg):
+            for _ in range(4 + steps // 4):
+                hdst.copy_(hsrc, non_blocking=True)
     ctx.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
@@ -57,7 +64,7 @@ def run(shape, B, steps, L=2, theta=1.0):
     k3 = ctx.profile_read(api.M.KERNEL_COMBINE)
     ms = e0.elapsed_time(e1)
     n = steps * L
-    out = dict(shape=shape, B=B, layer_us=round(ms * 1e3 / n, 2),
+    out = dict(shape=shape, B=B, pcie_load=pcie_load, layer_us=round(ms * 1e3 / n, 2),
                k2_us=round(k2["total_ms"] * 1e3 / max(1, k2["launches"]), 2),
                k2_launches_per_layer=k2["launches"] / n,
                k2_MB=round(k2["bytes"] / max(1, k2["launches"]) / 1e6, 2),
@@ -73,10 +80,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--cases", default="mixtral:1,qwen3:1,qwen3:4,qwen3:16,deepseek:1")
+    ap.add_argument("--pcie-load", action="store_true")
     args = ap.parse_args()
     for c in args.cases.split(","):
         shape, B = c.split(":")
-        print(json.dumps(run(shape, int(B), args.steps)), flush=True)
+        print(json.dumps(run(shape, int(B), args.steps, pcie_load=args.pcie_load)), flush=True)
 
 
 if __name__ == "__main__":
