@@ -240,14 +240,30 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
         }
       }
     }
+    // transpose reduction: at offset o each lane keeps one half of its values and adds the
+    // partner's copy of that half (NV-1 shuffles for NV values instead of 5 NV); afterwards lane
+    // l holds the warp sum of value l >> (5 - log2 NV); remaining offsets are a plain butterfly
+    {
+      constexpr int LOGV = NV >= 32 ? 5 : NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : 1;
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+      for (int st = 0; st < LOGV; ++st) {
+        const int o = 16 >> st;
+        const int half = NV >> (st + 1);
+        const bool upper = (lane & o) != 0;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) pv[v] += __shfl_xor_sync(0xffffffffu, pv[v], o);
+        for (int i = 0; i < half; ++i) {
+          const float send = upper ? pv[i] : pv[i + half];
+          const float keep = upper ? pv[i + half] : pv[i];
+          pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+#pragma unroll
+      for (int o = 16 >> LOGV; o; o >>= 1) pv[0] += __shfl_xor_sync(0xffffffffu, pv[0], o);
+    }
     float* rb = red + (size_t)(n & 1) * kConsumerWarps * NV;
-    if (lane == 0) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) rb[warp * NV + v] = pv[v];
+    {
+      constexpr int SH = NV >= 32 ? 0 : NV >= 16 ? 1 : NV >= 8 ? 2 : NV >= 4 ? 3 : 4;   // 5 - log2 NV
+      if ((lane & ((1 << SH) - 1)) == 0) rb[warp * NV + (lane >> SH)] = pv[0];
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&redbar[n & 1]);
