@@ -313,6 +313,58 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     phase2();
     flush(prev_seg, prev_ntok);
   }
+
+  // ---------------------------------------------------------------- fused combine (final launch)
+  if (p.combine) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(p.bar, 1ull);
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.bar) : "memory");
+        if (v < p.bar_target) __nanosleep(100);
+      } while (v < p.bar_target);
+      __threadfence();
+    }
+    __syncthreads();
+    // CTA c adds items [c W / G, (c+1) W / G) of the B x d/4 float4 outputs; each item sums its
+    // segments' per-CTA partials in K3's order (8 interleaved accumulators, then in order)
+    const int d4 = d >> 2;
+    const int64_t W = (int64_t)p.B * d4;
+    const int64_t lo = (int64_t)blockIdx.x * W / G, hi = (int64_t)(blockIdx.x + 1) * W / G;
+    for (int64_t q = lo + tid; q < hi; q += kThreads) {
+      const int b = (int)(q / d4);
+      const int c4 = (int)(q - (int64_t)b * d4);
+      const uint32_t bit = 1u << b;
+      float4 acc[8];
+#pragma unroll
+      for (int w2 = 0; w2 < 8; ++w2) acc[w2] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < p.ncomb; ++s) {
+        const CombineSeg sg = p.comb[s];
+        if (!(sg.tok_mask & bit)) continue;
+        const int ntok = __popc(sg.tok_mask);
+        const int t = __popc(sg.tok_mask & (bit - 1u));
+        const float4* base = reinterpret_cast<const float4*>(p.ws + sg.ws_off + (int64_t)t * d) + c4;
+        const int64_t stride4 = (int64_t)ntok * d4;
+        for (int ci = 0; ci < sg.nchunks; ++ci) {
+          const float4 v = base[(int64_t)ci * stride4];
+          float4& a = acc[ci & 7];
+          a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        }
+      }
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p.residual) {
+        const uint2 hv = reinterpret_cast<const uint2*>(p.h + (size_t)b * d)[c4];
+        r = make_float4(bf16lo(hv.x), bf16hi(hv.x), bf16lo(hv.y), bf16hi(hv.y));
+      }
+#pragma unroll
+      for (int w2 = 0; w2 < 8; ++w2) {
+        r.x += acc[w2].x; r.y += acc[w2].y; r.z += acc[w2].z; r.w += acc[w2].w;
+      }
+      reinterpret_cast<float4*>(p.y + (size_t)b * d)[c4] = r;
+    }
+  }
 }
 
 // The kernel parameter block is sized to the launch: kernel arguments travel in the launch
@@ -326,6 +378,11 @@ struct K2ParamsCap {
   int64_t total_rows;
   int d, K, nsegs;
   Seg segs[CAP];
+  int combine, B, residual, ncomb;
+  float* y;
+  unsigned long long* bar;
+  unsigned long long bar_target;
+  CombineSeg comb[CAP];
 };
 
 template <int TB, int CW, int RS, int CAP>
@@ -334,13 +391,23 @@ static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   q.h = p.h; q.ids = p.ids; q.w = p.w; q.ws = p.ws; q.total_rows = p.total_rows;
   q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
-  k2_split_expert<TB, CW, RS, K2ParamsCap<CAP>><<<grid, kThreads, k2_smem_bytes(p.d), s>>>(q);
+  q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0;
+  q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target;
+  for (int i = 0; i < q.ncomb; ++i) q.comb[i] = p.comb[i];
+  auto* fn = k2_split_expert<TB, CW, RS, K2ParamsCap<CAP>>;
+  if (p.combine) {   // grid barrier: every CTA must be co-resident
+    void* args[] = {&q};
+    cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, k2_smem_bytes(p.d), s);
+  } else {
+    fn<<<grid, kThreads, k2_smem_bytes(p.d), s>>>(q);
+  }
 }
 
 template <int TB, int CW, int RS>
 static void k2_launch_cap(const K2Params& p, int grid, cudaStream_t s) {
-  if (p.nsegs <= 8) k2_launch_t<TB, CW, RS, 8>(p, grid, s);
-  else if (p.nsegs <= 32) k2_launch_t<TB, CW, RS, 32>(p, grid, s);
+  const int n = p.combine && p.ncomb > p.nsegs ? p.ncomb : p.nsegs;
+  if (n <= 8) k2_launch_t<TB, CW, RS, 8>(p, grid, s);
+  else if (n <= 32) k2_launch_t<TB, CW, RS, 32>(p, grid, s);
   else k2_launch_t<TB, CW, RS, kMaxLaunchSegs>(p, grid, s);
 }
 

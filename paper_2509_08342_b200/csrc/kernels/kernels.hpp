@@ -32,7 +32,8 @@ struct RouterParams {
   int32_t* mb_ids;
   float* mb_w;
   int32_t* mb_rank;
-  volatile uint32_t* mb_seq;
+  volatile uint32_t* mb_seq_route;   // published after ids / weights
+  volatile uint32_t* mb_seq_rank;    // published after the next-layer ranking
   uint32_t seq;
   int B, d, N, K, renorm;
 };
@@ -50,6 +51,12 @@ struct Seg {
   int32_t pad;
 };
 
+struct CombineSeg {
+  int64_t ws_off;
+  int32_t nchunks;
+  uint32_t tok_mask;
+};
+
 struct K2Params {
   const uint16_t* h;      // [B][d]
   const int32_t* ids;     // [B][K]
@@ -58,6 +65,13 @@ struct K2Params {
   int64_t total_rows;
   int d, K, nsegs;
   Seg segs[kMaxLaunchSegs];
+  // fused combine (the step's final K2 launch, cooperative): after a grid barrier every CTA adds
+  // a slice of the step's partials in K3's fixed order
+  int combine, B, residual, ncomb;
+  float* y;
+  unsigned long long* bar;
+  unsigned long long bar_target;
+  CombineSeg comb[kMaxLaunchSegs];
 };
 // Partition rule shared with the host: CTA c of G owns launch rows [c*R/G, (c+1)*R/G).
 MOEPIC_HD inline int64_t k2_row_lo(int64_t c, int64_t R, int64_t G) { return c * R / G; }
@@ -67,11 +81,6 @@ size_t k2_smem_bytes(int d);
 void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s);
 
 // ------------------------------------------------------------------ K3: combine
-struct CombineSeg {
-  int64_t ws_off;
-  int32_t nchunks;
-  uint32_t tok_mask;
-};
 struct CombineParams {
   float* y;               // [B][d] fp32 out
   const uint16_t* h;      // residual source

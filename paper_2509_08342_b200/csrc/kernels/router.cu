@@ -1,11 +1,13 @@
 // K1 router + next-layer predictor (Eq. 2; Eq. 3).
 //
-// One warp per (matrix, token, expert) logit in fp64 canonical order C.R (R1): chunk
-// c of 8 consecutive k is lane c%32's; lanes add exact bf16*bf16 products in increasing k;
-// xor-butterfly 16,8,4,2,1.  The last CTA (ticket) selects the top-K per token by (logit desc,
-// id asc) with warp-shuffle argmax rounds, computes the Eq. 2 weights, ranks the next layer's
-// experts (reading Q9) and publishes ids / weights / ranking to device memory and to the
-// mapped-pinned mailbox (__threadfence_system, then seq).
+// Phase 1: one warp per (matrix, token, expert) logit in fp64 canonical order C.R (DESIGN.md
+// R1): chunk c of 8 consecutive k is lane c%32's; lanes add exact bf16*bf16 products in
+// increasing k; xor-butterfly 16,8,4,2,1.
+// Phase 2 (last CTA, ticket): top-K per token by (logit desc, id asc) with warp-shuffle argmax
+// rounds; Eq. 2 weights (one exp per lane); ids / weights published to device memory and to the
+// mapped-pinned mailbox, system fence, then `seq_route` — the host starts planning copies now.
+// Phase 3 (same CTA): batch ranking of the next layer's experts (reading Q9) by warp ballots
+// (rank_j = #experts whose key precedes j's), published with `seq_rank`.
 #include "kernels.hpp"
 #include "device_utils.cuh"
 
@@ -13,11 +15,6 @@
 
 namespace moepic {
 
-// ============================================================== K1 router
-struct Key {  // (value desc, id asc)
-  double v;
-  int id;
-};
 __device__ __forceinline__ bool key_better(double av, int aid, double bv, int bid) {
   return av > bv || (av == bv && aid < bid);
 }
@@ -27,17 +24,20 @@ __device__ __forceinline__ bool key_better(double av, int aid, double bv, int bi
 __device__ void warp_topk(const double* row, int N, int K, int* ids_out, unsigned* taken_bits) {
   const int lane = threadIdx.x & 31;
   unsigned taken = 0;  // bit q <-> expert lane + 32 q
+  double vals[kMaxN / 32];
+  for (int q = 0, j = lane; j < N; ++q, j += 32) vals[q] = row[j];
   for (int r = 0; r < K; ++r) {
     double bv = -INFINITY;
     int bid = 0x7fffffff;
-    for (int q = 0, j = lane; j < N; ++q, j += 32) {
-      if (taken & (1u << q)) continue;
-      double v = row[j];
-      if (key_better(v, j, bv, bid)) { bv = v; bid = j; }
+#pragma unroll
+    for (int q = 0; q < kMaxN / 32; ++q) {
+      const int j = lane + 32 * q;
+      if (j < N && !(taken & (1u << q)) && key_better(vals[q], j, bv, bid)) { bv = vals[q]; bid = j; }
     }
+#pragma unroll
     for (int o = 16; o; o >>= 1) {
-      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
       if (key_better(ov, oid, bv, bid)) { bv = ov; bid = oid; }
     }
     if ((bid & 31) == lane) taken |= 1u << (bid >> 5);
@@ -70,8 +70,9 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
       const uint4* hv = reinterpret_cast<const uint4*>(p.h + (size_t)b * p.d);
       const uint4* wv = reinterpret_cast<const uint4*>(W + (size_t)j * p.d);
       double acc = 0.0;
+#pragma unroll 4
       for (int c = lane; c < n_chunks; c += 32) {
-        uint4 a = __ldg(hv + c), w = __ldg(wv + c);
+        const uint4 a = __ldg(hv + c), w = __ldg(wv + c);
         float fa[8], fw[8];
         unpack8(a, fa);
         unpack8(w, fw);
@@ -83,11 +84,11 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
       if (lane == 0) p.logits[(size_t)m * BN + rem] = acc;
     }
   }
-  // ---- last CTA does the selection
+  // ---- the last CTA to finish phase 1 does the selection
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned t = atomicAdd(p.ticket, 1u);
+    const unsigned t = atomicAdd(p.ticket, 1u);
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
@@ -95,30 +96,43 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
   __threadfence();
   const double* L0 = p.logits;
   const double* L1 = p.logits + BN;
+
+  // ---- phase 2: routing
   if (p.W0 != nullptr) {
     for (int b = warp; b < p.B; b += nwarps) {
       unsigned bits;
-      warp_topk(L0 + (size_t)b * p.N, p.N, p.K, s_topk[warp], &bits);
+      const double* row = L0 + (size_t)b * p.N;
+      warp_topk(row, p.N, p.K, s_topk[warp], &bits);
       __syncwarp();
-      if (lane == 0) {
-        const double* row = L0 + (size_t)b * p.N;
-        double mx = row[s_topk[warp][0]];
-        double den = 0.0;
-        if (p.renorm) {
-          for (int k = 0; k < p.K; ++k) den += exp(row[s_topk[warp][k]] - mx);
-        } else {
-          for (int j = 0; j < p.N; ++j) den += exp(row[j] - mx);
-        }
-        for (int k = 0; k < p.K; ++k) {
-          int e = s_topk[warp][k];
-          float wk = (float)(exp(row[e] - mx) / den);
-          p.ids[b * p.K + k] = e;
-          p.w[b * p.K + k] = wk;
-        }
+      const double mx = row[s_topk[warp][0]];
+      double ek = 0.0, part = 0.0;
+      if (lane < p.K) ek = exp(row[s_topk[warp][lane]] - mx);
+      if (p.renorm) {
+        part = ek;
+      } else {
+        for (int j = lane; j < p.N; j += 32) part += exp(row[j] - mx);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane < p.K) {
+        p.ids[b * p.K + lane] = s_topk[warp][lane];
+        p.w[b * p.K + lane] = (float)(ek / part);
       }
       __syncwarp();
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < p.B * p.K; i += blockDim.x) {   // coalesced PCIe bursts
+      p.mb_ids[i] = p.ids[i];
+      p.mb_w[i] = p.w[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *p.mb_seq_route = p.seq;
+    }
   }
+
+  // ---- phase 3: next-layer ranking, key = (count desc, max logit desc, id asc)
   if (p.W1 != nullptr) {
     for (int j = threadIdx.x; j < p.N; j += blockDim.x) {
       s_cnt[j] = 0;
@@ -134,36 +148,31 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
         if (bits & (1u << q)) atomicAdd(&s_cnt[j], 1);
     }
     __syncthreads();
-    // rank_j = #{j' : key(j') before key(j)}, key = (count desc, max logit desc, id asc)
-    for (int j = threadIdx.x; j < p.N; j += blockDim.x) {
-      int r = 0;
+    for (int j = warp; j < p.N; j += nwarps) {
       const int cj = s_cnt[j];
       const double mj = s_max[j];
-      for (int o = 0; o < p.N; ++o) {
-        const int co = s_cnt[o];
-        const double mo = s_max[o];
-        r += (co > cj) || (co == cj && (mo > mj || (mo == mj && o < j)));
+      int r = 0;
+      for (int o0 = 0; o0 < p.N; o0 += 32) {
+        const int o = o0 + lane;
+        bool before = false;
+        if (o < p.N) {
+          const int co = s_cnt[o];
+          const double mo = s_max[o];
+          before = (co > cj) || (co == cj && (mo > mj || (mo == mj && o < j)));
+        }
+        r += __popc(__ballot_sync(0xffffffffu, before));
       }
-      p.ranking[r] = j;
+      if (lane == 0) p.ranking[r] = j;
     }
-  }
-  __syncthreads();
-  // publish to the mapped-pinned mailbox in coalesced bursts (consecutive threads -> consecutive
-  // words, so a warp's writes merge into few PCIe transactions), one system fence, then seq
-  if (p.W0 != nullptr) {
-    for (int i = threadIdx.x; i < p.B * p.K; i += blockDim.x) {
-      p.mb_ids[i] = p.ids[i];
-      p.mb_w[i] = p.w[i];
-    }
-  }
-  if (p.W1 != nullptr)
+    __syncthreads();
     for (int i = threadIdx.x; i < p.N; i += blockDim.x) p.mb_rank[i] = p.ranking[i];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *p.ticket = 0u;
-    __threadfence_system();
-    *p.mb_seq = p.seq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *p.mb_seq_rank = p.seq;
+    }
   }
+  if (threadIdx.x == 0) *p.ticket = 0u;
 }
 
 void launch_router(const RouterParams& p, cudaStream_t s) {

@@ -206,6 +206,7 @@ struct moepic_ctx {
   Plan pending;
   int last_buf = 1;
   uint32_t seq = 0;
+  uint64_t bar_base = 0;             // grid-barrier arrivals so far (fused combine)
   bool poisoned = false;
   std::string err;
   moepic_counters ctr{};
@@ -493,8 +494,15 @@ struct StepSeg {
   int32_t row0;     // first intermediate index of the segment inside its expert
 };
 
+struct FuseCombine {
+  float* y;
+  int residual;
+  bool done;
+};
+
 static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& segs, const uint16_t* h, int B,
-                                  cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb, int& launches) {
+                                  cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb, int& launches,
+                                  FuseCombine* fuse = nullptr) {
   const int d = ctx->desc.d;
   const int tbmax = k2_max_tokens(d);
   // split by token groups of <= tbmax tokens
@@ -563,6 +571,20 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
     while (tb < maxtok) tb <<= 1;
     uint64_t alg_bytes = (uint64_t)R * ctx->rb();
     for (size_t i = i0; i < i1; ++i) alg_bytes += (uint64_t)__builtin_popcount(work[i].mask) * d * 2;
+    // the last launch of the step's last group also combines (grid barrier, no K3 launch)
+    kp.combine = 0;
+    if (fuse && i1 == work.size() && comb.size() <= (size_t)kMaxLaunchSegs) {
+      kp.combine = 1;
+      kp.B = B;
+      kp.residual = fuse->residual;
+      kp.y = fuse->y;
+      kp.ncomb = (int)comb.size();
+      for (size_t i = 0; i < comb.size(); ++i) kp.comb[i] = comb[i];
+      kp.bar = reinterpret_cast<unsigned long long*>(ctx->arena + ctx->lay.ticket + 8);
+      ctx->bar_base += (uint64_t)G;
+      kp.bar_target = ctx->bar_base;
+      fuse->done = true;
+    }
     const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
     launch_k2(kp, (int)G, tb, s);
     ctx->prof_end(pe, s, alg_bytes);
@@ -573,8 +595,8 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
   return MOEPIC_OK;
 }
 
-static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s) {
-  volatile uint32_t* seqp = reinterpret_cast<volatile uint32_t*>(ctx->mailbox);
+static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s, size_t off) {
+  volatile uint32_t* seqp = reinterpret_cast<volatile uint32_t*>(ctx->mailbox + off);
   auto t0 = std::chrono::steady_clock::now();
   uint64_t spins = 0;
   while (*seqp != ctx->seq) {
@@ -605,6 +627,8 @@ static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s) {
   return MOEPIC_OK;
 }
 
+static moepic_status read_ranking(moepic_ctx* ctx, cudaStream_t s);
+
 static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int layer_route, int layer_pred,
                                 cudaStream_t s, bool read_ids, bool read_rank) {
   const auto& d = ctx->desc;
@@ -618,7 +642,8 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   rp.ranking = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.ranking);
   rp.ticket = reinterpret_cast<unsigned int*>(ctx->arena + ctx->lay.ticket);
   uint8_t* mb = ctx->mailbox_dev;
-  rp.mb_seq = reinterpret_cast<volatile uint32_t*>(mb);
+  rp.mb_seq_route = reinterpret_cast<volatile uint32_t*>(mb);
+  rp.mb_seq_rank = reinterpret_cast<volatile uint32_t*>(mb + 4);
   rp.mb_ids = reinterpret_cast<int32_t*>(mb + 64);
   rp.mb_w = reinterpret_cast<float*>(mb + 64 + (size_t)d.max_batch * d.K * 4);
   rp.mb_rank = reinterpret_cast<int32_t*>(mb + 64 + (size_t)d.max_batch * d.K * 8);
@@ -629,14 +654,24 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
   CK(cudaGetLastError());
   ctx->ctr.kernel_launches++;
-  moepic_status st = wait_mailbox(ctx, s);
-  if (st != MOEPIC_OK) return st;
   const uint8_t* hb = ctx->mailbox;
   if (read_ids) {
+    moepic_status st = wait_mailbox(ctx, s, 0);
+    if (st != MOEPIC_OK) return st;
     memcpy(ctx->ids_h.data(), hb + 64, (size_t)B * d.K * 4);
     memcpy(ctx->w_h.data(), hb + 64 + (size_t)d.max_batch * d.K * 4, (size_t)B * d.K * 4);
   }
-  if (read_rank) memcpy(ctx->rank_h.data(), hb + 64 + (size_t)d.max_batch * d.K * 8, (size_t)d.N * 4);
+  if (read_rank) return read_ranking(ctx, s);
+  return MOEPIC_OK;
+}
+
+// The next-layer ranking is published after the routing; the step plans its prefetch only at
+// the end, so the host waits for it late (usually already there).
+static moepic_status read_ranking(moepic_ctx* ctx, cudaStream_t s) {
+  moepic_status st = wait_mailbox(ctx, s, 4);
+  if (st != MOEPIC_OK) return st;
+  const auto& d = ctx->desc;
+  memcpy(ctx->rank_h.data(), ctx->mailbox + 64 + (size_t)d.max_batch * d.K * 8, (size_t)d.N * 4);
   return MOEPIC_OK;
 }
 
@@ -867,7 +902,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   const int buf = have_plan ? used.buf : (ctx->last_buf ^ 1);
 
   // ---- K1 (router + fused next-layer predictor) and the mailbox handoff
-  moepic_status st = run_router(ctx, h, B, layer, predict ? j : -1, s, true, predict);
+  moepic_status st = run_router(ctx, h, B, layer, predict ? j : -1, s, true, false);
   if (st != MOEPIC_OK) return st;
   ++launches;
 
@@ -964,18 +999,21 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   // ---- K2 launches: resident now / prefetched / on-demand, then the combine
   int64_t ws_next = 0;
   std::vector<CombineSeg> comb;
-  st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches);
+  FuseCombine fuse{y_dev, ((flags & MOEPIC_RESIDUAL) && d.ep_rank == 0) ? 1 : 0, false};
+  const bool lastA = gB.empty() && gC.empty(), lastB = gC.empty();
+  st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches, lastA ? &fuse : nullptr);
   if (st != MOEPIC_OK) return st;
   if (!gB.empty()) {
     CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
-    st = launch_group(ctx, gB, h, B, s, ws_next, comb, launches);
+    st = launch_group(ctx, gB, h, B, s, ws_next, comb, launches, lastB ? &fuse : nullptr);
     if (st != MOEPIC_OK) return st;
   }
   if (!gC.empty()) {
     CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
-    st = launch_group(ctx, gC, h, B, s, ws_next, comb, launches);
+    st = launch_group(ctx, gC, h, B, s, ws_next, comb, launches, &fuse);
     if (st != MOEPIC_OK) return st;
   }
+  if (!fuse.done) {   // no K2 launch fused the combine (no segments, or too many): run K3
   if (comb.size() > (size_t)kMaxStepSegs) return fail(&ctx->err, MOEPIC_ERUNTIME, "too many segments in one step");
   static CombineParams cpar;
   cpar.y = y_dev;
@@ -996,6 +1034,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   CK(cudaGetLastError());
   ++launches;
   }
+  }
   // alpha experts that arrived as full prefetches and were admitted: D2D their top rows
   for (const auto& a : res.adm) {
     if (!a.d2d_from_plan || a.victim == kAdmNone || l.I_top == 0) continue;
@@ -1011,6 +1050,8 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   // ---- next-layer prefetch, issued after this layer's on-demand copies
   Plan next;
   if (predict) {
+    st = read_ranking(ctx, s);
+    if (st != MOEPIC_OK) return st;
     cp.make_plan(j, ctx->rank_h.data(), next);
     st = issue_plan(ctx, next, buf ^ 1);
     if (st != MOEPIC_OK) return st;

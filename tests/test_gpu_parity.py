@@ -259,3 +259,33 @@ def test_residual_flag_and_errors():
     with pytest.raises(api.MoEpicError):
         ctx.configure(v_e=5.0)                     # exceeds v_e_max
     ctx.layer_forward(1, h.cuda(), y)              # still usable after EINVAL
+
+
+def test_cancel_prefetch_same_results_fewer_bytes():
+    """P:291 "terminates the prefetch": dropping the unissued chunks of mispredicted experts
+    changes neither traces nor outputs, only the bytes moved (<= planned)."""
+    api = _api()
+    S = synth.SHAPES["qwen3"]
+    runs = {}
+    for cancel in (True, False):
+        m = Model(3, S.N, S.K, S.d, S.I, L_host=1, seed=2, gen_device="cuda")
+        ctx = _ctx(m, v_e_max=96.0)
+        ctx.configure(v_e=96.0, seed=1, cancel_prefetch=cancel, y_cap_i=[16] * 3)
+        H = synth.hidden_states(2, 12, 3, S.d)
+        ys, trs = [], []
+        for t in range(12):
+            for i in range(3):
+                y = torch.empty(1, S.d, dtype=torch.float32, device="cuda")
+                tr = ctx.layer_forward(i, H[t, i][None].cuda(), y, flags=api.M.FUSE_PREDICT)
+                torch.cuda.synchronize()
+                ys.append(y.cpu().numpy())
+                trs.append((tr.act, tr.adm, tr.plan, tr.pcie_prefetch))
+        runs[cancel] = (ys, trs, ctx.counters())
+        ctx.close()
+    assert runs[True][1] == runs[False][1]
+    for a, b in zip(runs[True][0], runs[False][0]):
+        np.testing.assert_array_equal(a, b)            # deterministic kernels: bit-identical
+    c_on, c_off = runs[True][2], runs[False][2]
+    assert c_off["pcie_prefetch_bytes"] == c_off["pcie_prefetch_planned_bytes"]
+    assert c_on["pcie_prefetch_planned_bytes"] == c_off["pcie_prefetch_planned_bytes"]
+    assert c_on["pcie_prefetch_bytes"] < c_on["pcie_prefetch_planned_bytes"]
