@@ -29,11 +29,12 @@ struct RouterParams {
   int32_t* ranking;       // [N] out
   unsigned int* ticket;   // zero-initialised, reset by the kernel
   // mapped pinned mailbox (device aliases)
-  int32_t* mb_ids;
-  float* mb_w;
-  int32_t* mb_rank;
-  volatile uint32_t* mb_seq_route;   // published after ids / weights
-  volatile uint32_t* mb_seq_rank;    // published after the next-layer ranking
+  // mapped-pinned mailbox of self-validating 64-bit words: (seq << 32) | payload32.  The host
+  // accepts a word once its tag equals seq, so no system-scope fence is needed (a fence.sys
+  // waits behind the saturated host->device link).  Layout: ids [B*K], w bits [B*K], rank [N].
+  unsigned long long* mb_ids;
+  unsigned long long* mb_w;
+  unsigned long long* mb_rank;
   uint32_t seq;
   int B, d, N, K, renorm;
 };

@@ -121,14 +121,10 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
       __syncwarp();
     }
     __syncthreads();
+    const unsigned long long tag = (unsigned long long)p.seq << 32;
     for (int i = threadIdx.x; i < p.B * p.K; i += blockDim.x) {   // coalesced PCIe bursts
-      p.mb_ids[i] = p.ids[i];
-      p.mb_w[i] = p.w[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      *p.mb_seq_route = p.seq;
+      p.mb_ids[i] = tag | (uint32_t)p.ids[i];
+      p.mb_w[i] = tag | __float_as_uint(p.w[i]);
     }
   }
 
@@ -165,12 +161,8 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
       if (lane == 0) p.ranking[r] = j;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < p.N; i += blockDim.x) p.mb_rank[i] = p.ranking[i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      *p.mb_seq_rank = p.seq;
-    }
+    const unsigned long long tag = (unsigned long long)p.seq << 32;
+    for (int i = threadIdx.x; i < p.N; i += blockDim.x) p.mb_rank[i] = tag | (uint32_t)p.ranking[i];
   }
   if (threadIdx.x == 0) *p.ticket = 0u;
 }

@@ -377,7 +377,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
     cudaGetLastError();
     return bail(MOEPIC_ENOMEM);
   }
-  const size_t mb_bytes = 64 + (size_t)desc->max_batch * desc->K * 8 + (size_t)desc->N * 4;
+  const size_t mb_bytes = 64 + ((size_t)desc->max_batch * desc->K * 2 + (size_t)desc->N) * 8;
   if (cudaHostAlloc(&ctx->mailbox, mb_bytes, cudaHostAllocMapped) != cudaSuccess) return bail(MOEPIC_ENOMEM);
   memset(ctx->mailbox, 0, mb_bytes);
   if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->mailbox_dev), ctx->mailbox, 0) != cudaSuccess)
@@ -595,11 +595,18 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
   return MOEPIC_OK;
 }
 
-static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s, size_t off) {
-  volatile uint32_t* seqp = reinterpret_cast<volatile uint32_t*>(ctx->mailbox + off);
+// Spin until the n tagged mailbox words starting at word index w0 all carry ctx->seq (each
+// 64-bit word is written atomically by the router kernel: (seq << 32) | payload), pumping the
+// prefetch feed meanwhile.  No system fence is involved on either side.
+static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s, size_t w0, size_t n) {
+  volatile const uint64_t* words = reinterpret_cast<volatile const uint64_t*>(ctx->mailbox + 64) + w0;
+  const uint64_t want = ctx->seq;
   auto t0 = std::chrono::steady_clock::now();
   uint64_t spins = 0;
-  while (*seqp != ctx->seq) {
+  size_t ok = 0;   // words [0, ok) already verified
+  for (;;) {
+    while (ok < n && (words[ok] >> 32) == want) ++ok;
+    if (ok == n) break;
 #if defined(__x86_64__)
     __builtin_ia32_pause();
 #endif
@@ -613,9 +620,14 @@ static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s, size_t off) {
         ctx->poisoned = true;
         return fail(&ctx->err, MOEPIC_ERUNTIME, "router kernel failed: %s", cudaGetErrorString(q));
       }
-      if (q == cudaSuccess && *seqp != ctx->seq) {
-        ctx->poisoned = true;
-        return fail(&ctx->err, MOEPIC_ERUNTIME, "router mailbox not published");
+      if (q == cudaSuccess) {   // kernel done: every word must be there now
+        std::atomic_thread_fence(std::memory_order_acquire);
+        while (ok < n && (words[ok] >> 32) == want) ++ok;
+        if (ok != n) {
+          ctx->poisoned = true;
+          return fail(&ctx->err, MOEPIC_ERUNTIME, "router mailbox not published");
+        }
+        break;
       }
       if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
         ctx->poisoned = true;
@@ -642,11 +654,10 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   rp.ranking = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.ranking);
   rp.ticket = reinterpret_cast<unsigned int*>(ctx->arena + ctx->lay.ticket);
   uint8_t* mb = ctx->mailbox_dev;
-  rp.mb_seq_route = reinterpret_cast<volatile uint32_t*>(mb);
-  rp.mb_seq_rank = reinterpret_cast<volatile uint32_t*>(mb + 4);
-  rp.mb_ids = reinterpret_cast<int32_t*>(mb + 64);
-  rp.mb_w = reinterpret_cast<float*>(mb + 64 + (size_t)d.max_batch * d.K * 4);
-  rp.mb_rank = reinterpret_cast<int32_t*>(mb + 64 + (size_t)d.max_batch * d.K * 8);
+  const size_t BK = (size_t)d.max_batch * d.K;
+  rp.mb_ids = reinterpret_cast<unsigned long long*>(mb + 64);
+  rp.mb_w = rp.mb_ids + BK;
+  rp.mb_rank = rp.mb_w + BK;
   rp.seq = ++ctx->seq;
   rp.B = B; rp.d = d.d; rp.N = d.N; rp.K = d.K; rp.renorm = d.renorm_topk;
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_ROUTER);
@@ -654,12 +665,17 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
   CK(cudaGetLastError());
   ctx->ctr.kernel_launches++;
-  const uint8_t* hb = ctx->mailbox;
   if (read_ids) {
-    moepic_status st = wait_mailbox(ctx, s, 0);
+    const size_t n = (size_t)B * d.K;
+    moepic_status st = wait_mailbox(ctx, s, 0, n);
+    if (st == MOEPIC_OK) st = wait_mailbox(ctx, s, BK, n);
     if (st != MOEPIC_OK) return st;
-    memcpy(ctx->ids_h.data(), hb + 64, (size_t)B * d.K * 4);
-    memcpy(ctx->w_h.data(), hb + 64 + (size_t)d.max_batch * d.K * 4, (size_t)B * d.K * 4);
+    const uint64_t* words = reinterpret_cast<const uint64_t*>(ctx->mailbox + 64);
+    for (size_t i = 0; i < n; ++i) {
+      ctx->ids_h[i] = (int32_t)(uint32_t)words[i];
+      const uint32_t wb = (uint32_t)words[BK + i];
+      memcpy(&ctx->w_h[i], &wb, 4);
+    }
   }
   if (read_rank) return read_ranking(ctx, s);
   return MOEPIC_OK;
@@ -668,10 +684,12 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
 // The next-layer ranking is published after the routing; the step plans its prefetch only at
 // the end, so the host waits for it late (usually already there).
 static moepic_status read_ranking(moepic_ctx* ctx, cudaStream_t s) {
-  moepic_status st = wait_mailbox(ctx, s, 4);
-  if (st != MOEPIC_OK) return st;
   const auto& d = ctx->desc;
-  memcpy(ctx->rank_h.data(), ctx->mailbox + 64 + (size_t)d.max_batch * d.K * 8, (size_t)d.N * 4);
+  const size_t off = 2 * (size_t)d.max_batch * d.K;
+  moepic_status st = wait_mailbox(ctx, s, off, (size_t)d.N);
+  if (st != MOEPIC_OK) return st;
+  const uint64_t* words = reinterpret_cast<const uint64_t*>(ctx->mailbox + 64) + off;
+  for (int i = 0; i < d.N; ++i) ctx->rank_h[i] = (int32_t)(uint32_t)words[i];
   return MOEPIC_OK;
 }
 
