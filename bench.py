@@ -38,9 +38,9 @@ METRIC_PREFILL = "MoE-layer prefill throughput at 50% expert VRAM budget (tokens
 
 CONFIGS = {
     # name: (shape, L, L_host, B, v_e fraction, theta)
-    "mixtral": dict(shape="mixtral", L=32, L_host=2, B=1, budget=0.5, theta=0.5),
+    "mixtral": dict(shape="mixtral", L=32, L_host=2, B=1, budget=0.5, theta=0.5, adaptive=True),
     "qwen3": dict(shape="qwen3", L=48, L_host=4, B=1, budget=0.5, theta=0.5, adaptive=True),
-    "deepseek": dict(shape="deepseek", L=26, L_host=4, B=1, budget=0.5, theta=0.5),
+    "deepseek": dict(shape="deepseek", L=26, L_host=4, B=1, budget=0.5, theta=0.5, adaptive=True),
     "toy": dict(shape="toy", L=2, L_host=2, B=1, budget=0.25, theta=0.5),
     # BJ configs[4]: Mixtral-shaped prefill of 2048 tokens through a 4-layer stack (tcgen05 GEMMs)
     "mixtral_prefill": dict(shape="mixtral", L=4, L_host=2, B=2048, budget=0.5, theta=0.5, prefill=True),
@@ -424,7 +424,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=None, help="override the config's decode batch")
-    ap.add_argument("--tau", type=int, default=128, help="tokens per Alg. 1 period (adaptive configs)")
+    ap.add_argument("--tau", type=int, default=64, help="tokens per Alg. 1 period (adaptive configs)")
     ap.add_argument("--no-adapt", action="store_true", help="keep the uniform theta = 0.5 layout")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
