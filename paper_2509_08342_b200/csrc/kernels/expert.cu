@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
         for (int t = 0; t < TB; ++t) {
           const float a = act_prev[r][t];
 #pragma unroll
-          for (int c = 0; c < CW; ++c) yacc[t][c] = fmaf(a, dn[c], yacc[t][c]);
+          for (int c = 0; c < CW; c += 2) fma2(yacc[t][c], yacc[t][c + 1], a, a, dn[c], dn[c + 1]);
         }
       }
     }
@@ -220,9 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     const uint8_t* tile = stages + (size_t)st * tileb;
 
     // ---- phase 1: partial gate / up dots
-    float pv[NV];
+    // even / odd column partials so consecutive columns pair up in one FFMA2
+    float pv[NV], po[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) pv[v] = 0.f;
+    for (int v = 0; v < NV; ++v) pv[v] = po[v] = 0.f;
     if (owns) {
 #pragma unroll
       for (int r = 0; r < RS; ++r) {
@@ -233,13 +234,16 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
 #pragma unroll
           for (int t = 0; t < TB; ++t)
 #pragma unroll
-            for (int c = 0; c < CW; ++c) {
-              pv[r * TB + t] = fmaf(g[c], hreg[t][c], pv[r * TB + t]);
-              pv[RS * TB + r * TB + t] = fmaf(u[c], hreg[t][c], pv[RS * TB + r * TB + t]);
+            for (int c = 0; c < CW; c += 2) {
+              fma2(pv[r * TB + t], po[r * TB + t], g[c], g[c + 1], hreg[t][c], hreg[t][c + 1]);
+              fma2(pv[RS * TB + r * TB + t], po[RS * TB + r * TB + t], u[c], u[c + 1], hreg[t][c],
+                   hreg[t][c + 1]);
             }
         }
       }
     }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) pv[v] += po[v];
     // transpose reduction: at offset o each lane keeps one half of its values and adds the
     // partner's copy of that half (NV-1 shuffles for NV values instead of 5 NV); afterwards lane
     // l holds the warp sum of value l >> (5 - log2 NV); remaining offsets are a plain butterfly
