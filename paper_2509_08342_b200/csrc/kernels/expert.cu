@@ -232,13 +232,22 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
           load_row(tile + (size_t)r * rowb, g);
           load_row(tile + (size_t)r * rowb + 2 * d, u);
 #pragma unroll
-          for (int t = 0; t < TB; ++t)
+          for (int t = 0; t < TB; ++t) {
+            if constexpr (TB <= 2) {   // FFMA2 needs the odd partials: only where registers allow
 #pragma unroll
-            for (int c = 0; c < CW; c += 2) {
-              fma2(pv[r * TB + t], po[r * TB + t], g[c], g[c + 1], hreg[t][c], hreg[t][c + 1]);
-              fma2(pv[RS * TB + r * TB + t], po[RS * TB + r * TB + t], u[c], u[c + 1], hreg[t][c],
-                   hreg[t][c + 1]);
+              for (int c = 0; c < CW; c += 2) {
+                fma2(pv[r * TB + t], po[r * TB + t], g[c], g[c + 1], hreg[t][c], hreg[t][c + 1]);
+                fma2(pv[RS * TB + r * TB + t], po[RS * TB + r * TB + t], u[c], u[c + 1], hreg[t][c],
+                     hreg[t][c + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < CW; ++c) {
+                pv[r * TB + t] = fmaf(g[c], hreg[t][c], pv[r * TB + t]);
+                pv[RS * TB + r * TB + t] = fmaf(u[c], hreg[t][c], pv[RS * TB + r * TB + t]);
+              }
             }
+          }
         }
       }
     }
