@@ -158,11 +158,11 @@ def run_ours(args, log):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())   # ranks may share a GPU (gloo test)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
     cfg = CONFIGS[args.config]
     pcie = pcie_probe(torch)
     log(f"[bench] pinned H2D probe {pcie:.2f} GB/s")
@@ -257,16 +257,34 @@ def run_ours(args, log):
         Hh = [[synth.bf16_bits(H[i, t * B:(t + 1) * B].cpu()) for i in range(L)] for t in range(T, T + args.e2e_steps)]
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            # EP: the host-buffer call returns this rank's partial y, so stage through pinned
+            # buffers explicitly and combine on the device before the D2H read
+            hp = [[torch.from_numpy(Hh[t][i].view(np.int16)).pin_memory() for i in range(L)] for t in range(args.e2e_steps)]
+            yp = torch.empty(B, S.d, dtype=torch.float32).pin_memory()
+            hd = torch.empty(B, S.d, dtype=torch.int16, device="cuda")
+            dist.barrier()
         e0.record(stream)
         for t in range(args.e2e_steps):
             for i in range(L):
-                yh, _ = ctx.layer_forward_host(i, Hh[t][i], stream=stream, flags=F, trace=False)
+                if dist:
+                    with torch.cuda.stream(stream):
+                        hd.copy_(hp[t][i], non_blocking=True)
+                        ctx.layer_forward(i, hd.view(torch.bfloat16), y, stream=stream, flags=F, trace=False)
+                        dist.all_reduce(y)
+                        yp.copy_(y, non_blocking=True)
+                else:
+                    yh, _ = ctx.layer_forward_host(i, Hh[t][i], stream=stream, flags=F, trace=False)
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
+        if dist:
+            tt = torch.tensor([ems], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
         e2e = {"value": round(args.e2e_steps * B / (ems / 1e3), 4), "unit": "tokens/s",
                "h2d_bytes_per_step": L * B * S.d * 2, "d2h_bytes_per_step": L * B * S.d * 4,
-               "api": "moepic_layer_forward_host"}
+               "api": "moepic_layer_forward + all_reduce (pinned staging)" if dist else "moepic_layer_forward_host"}
 
     peaks = _peaks()
     hbm_peak = float(peaks["hbm_gbs"])
@@ -295,8 +313,7 @@ def run_ours(args, log):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded random weights, organic routing process; synth/)",
-        "config": {"workload": f"{cfg['shape']}-shaped {'prefill' if prefill else 'decode'}, B={B}, "
-                               f"{cfg['budget']:.0%} expert VRAM budget",
+        "config": {"workload": _workload(cfg),
                    "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
                    "global_batch": B, "seq_len": 1, "parallelism": f"ep{world}" if world > 1 else "single",
                    "v_e_experts": v_e, "theta": cfg["theta"], "policy": "LCP", "y_cap": S.K * B,
@@ -329,6 +346,11 @@ def run_ours(args, log):
     if dist:
         dist.destroy_process_group()
     return out if rank == 0 else None
+
+
+def _workload(cfg):
+    kind = "prefill" if cfg.get("prefill") else "decode"
+    return f"{cfg['shape']}-shaped {kind}, B={cfg['B']}, {cfg['budget']:.0%} expert VRAM budget"
 
 
 def _oracle_layer_step(S, cfg, keep_bits, h_bits, router_bits):
@@ -388,28 +410,31 @@ def run_reference(args, log):
     for e in range(S.N):
         keep[e] = tuple(synth.bf16_bits(x) for x in synth.expert_weights(0, 0, e, S.d, S.I, device=dev))
     router = synth.bf16_bits(synth.router_weights(0, 0, S.N, S.d))
-    H = synth.hidden_states(1, args.warmup + args.steps, 1, S.d)
+    prefill = bool(cfg.get("prefill"))
+    nt = min(cfg["B"], 64)                     # tokens per sampled layer step (prefill: 64 of B)
+    H = synth.hidden_states(1, (args.warmup + args.steps) * nt, 1, S.d)
     for t in range(args.warmup):
-        _oracle_layer_step(S, cfg, keep, synth.bf16_bits(H[t, 0][None]), router)
+        _oracle_layer_step(S, cfg, keep, synth.bf16_bits(H[t * nt:(t + 1) * nt, 0]), router)
     t0 = time.perf_counter()
     for t in range(args.warmup, args.warmup + args.steps):
-        _oracle_layer_step(S, cfg, keep, synth.bf16_bits(H[t, 0][None]), router)
+        _oracle_layer_step(S, cfg, keep, synth.bf16_bits(H[t * nt:(t + 1) * nt, 0]), router)
     dt = time.perf_counter() - t0
     per_layer = dt / args.steps
-    value = 1.0 / (per_layer * cfg["L"])
+    value = nt / (per_layer * cfg["L"])
     try:
         from threadpoolctl import threadpool_info
         cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "tokens/s", "n_gpus": 0,
+    return {"impl": "reference", "metric": METRIC_PREFILL if prefill else METRIC, "value": round(value, 6),
+            "unit": "tokens/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_layer * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random weights)",
-            "config": {"workload": f"{args.config}-shaped decode, B=1, one layer step per bench step",
-                       "layers_extrapolated": cfg["L"]},
+            "config": {"workload": _workload(cfg), "sample_tokens_per_step": nt, "layers_extrapolated": cfg["L"]},
             "cpu_baseline": {"value": round(value, 6), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{args.steps} single-token layer steps (layer 0), x{cfg['L']} layers",
+                             "sample": f"{args.steps} layer steps of {nt} token(s) (layer 0, all experts resident), "
+                                       f"x{cfg['L']} layers",
                              "cpu": _cpu_name()},
             "e2e": {"value": round(value, 6), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -426,6 +451,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="override the config's decode batch")
     ap.add_argument("--tau", type=int, default=64, help="tokens per Alg. 1 period (adaptive configs)")
     ap.add_argument("--no-adapt", action="store_true", help="keep the uniform theta = 0.5 layout")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets several ranks share one GPU (multi-rank test on a 1-GPU box)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.batch:
