@@ -47,6 +47,18 @@ CONFIGS = {
 }
 
 
+# NEXT-1 ablation modes on the same engine
+MODES = {
+    "moepic": {},                                                   # LCP + SP + CCA (Alg. 1 if adaptive)
+    "no-cca": dict(adaptive=False),                                 # uniform V_i, theta = 0.5
+    "no-lcp": dict(policy="RND"),                                   # random replacement
+    "cache-only": dict(theta=1.0, prefetch=False, adaptive=False),  # theta = 1, no prefetch
+    "prefetch-only": dict(v_e=0.0, adaptive=False),                 # V_i = 0
+    "lru-prefetch": dict(theta=1.0, policy="LRU", adaptive=False),  # ~ Mixtral-offloading / AdapMoE
+    "lfu-prefetch": dict(theta=1.0, policy="LFU", adaptive=False),  # ~ MoE-Infinity
+}
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -170,6 +182,16 @@ def run_ours(args, log):
     L, B = cfg["L"], cfg["B"]
     t0 = time.time()
     base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
+    mode = MODES[args.mode]
+    if "theta" in mode:
+        base_cfg["theta_i"] = [mode["theta"]] * L
+    for k in ("policy", "prefetch"):
+        if k in mode:
+            base_cfg[k] = getattr(api.M, mode[k]) if k == "policy" else mode[k]
+    if "v_e" in mode:
+        base_cfg["v_e"] = mode["v_e"]
+    if mode.get("adaptive") is False:
+        cfg["adaptive"] = False
     ctx.configure(**base_cfg)
     log(f"[bench] configure (re-layout {v_e:.0f} tops) {time.time() - t0:.1f}s")
     adapt_tokens = 2 * args.tau if cfg.get("adaptive") else 0
@@ -191,7 +213,37 @@ def run_ours(args, log):
             with torch.cuda.stream(stream):
                 dist.all_reduce(y)      # EP combine: sum of per-rank partial outputs
 
-    step = token_ep if world > 1 else token
+    # EP prefill: T/G tokens per rank.  Each rank gathers the batch
+    # (all-gather of bf16 rows), runs the replicated router and its own expert block over every
+    # token, and a reduce-scatter returns each rank the summed fp32 rows of its own T/G tokens.
+    Bl = B // world
+    hfull = torch.empty(B, S.d, dtype=torch.bfloat16, device="cuda")
+    ylocal = torch.empty(Bl, S.d, dtype=torch.float32, device="cuda")
+    nccl = args.dist_backend == "nccl"
+
+    def token_ep_prefill(t):
+        for i in range(L):
+            with torch.cuda.stream(stream):
+                hl = H[i, t * B + rank * Bl:t * B + (rank + 1) * Bl]
+                if nccl:
+                    dist.all_gather_into_tensor(hfull, hl)
+                else:                       # gloo test mode: stage through the host
+                    parts = [torch.empty(Bl, S.d, dtype=torch.bfloat16) for _ in range(world)]
+                    dist.all_gather(parts, hl.cpu())
+                    hfull.copy_(torch.cat(parts))
+                ctx.layer_forward(i, hfull, y, stream=stream, flags=F, trace=False)
+                if nccl:
+                    dist.reduce_scatter_tensor(ylocal, y)
+                else:
+                    yc = y.cpu()
+                    dist.all_reduce(yc)
+                    ylocal.copy_(yc[rank * Bl:(rank + 1) * Bl])
+
+    if world > 1 and cfg.get("prefill"):
+        assert B % world == 0, "prefill batch must divide by the EP size"
+        step = token_ep_prefill
+    else:
+        step = token_ep if world > 1 else token
     solved = None
     if adapt_tokens:
         # Alg. 1 outer loop: run 2 tau tokens on the uniform theta = 0.5 layout, profile
@@ -316,7 +368,11 @@ def run_ours(args, log):
         "config": {"workload": _workload(cfg),
                    "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
                    "global_batch": B, "seq_len": 1, "parallelism": f"ep{world}" if world > 1 else "single",
-                   "v_e_experts": v_e, "theta": cfg["theta"], "policy": "LCP", "y_cap": S.K * B,
+                   "ep_collectives": None if world == 1 else (
+                       "all_gather(h) + reduce_scatter(y), T/G tokens per rank" if prefill else "all_reduce(y)"),
+                   "v_e_experts": base_cfg["v_e"], "theta": base_cfg["theta_i"][0], "mode": args.mode,
+                   "policy": MODES[args.mode].get("policy", "LCP"), "prefetch": base_cfg.get("prefetch", True),
+                   "y_cap": S.K * B,
                    "alg1": None if solved is None else {"tau_tokens": args.tau, "theta_eff_min": min(solved["theta_eff_i"]),
                                                         "theta_eff_max": max(solved["theta_eff_i"]),
                                                         "C_min": min(solved["C_i"]), "C_max": max(solved["C_i"])},
@@ -381,7 +437,18 @@ def cpu_baseline(keep, S, cfg, args, log, n_layer_steps=3):
         _oracle_layer_step(S, cfg, keep, hb, router)
         ts.append(time.perf_counter() - t0)
     per_layer = statistics.mean(ts)
+    one = None
+    try:                                   # BLAS pinned to one thread, one layer step
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            hb = synth.bf16_bits(H[:nt, 0])
+            t0 = time.perf_counter()
+            _oracle_layer_step(S, cfg, keep, hb, router)
+            one = round(nt / ((time.perf_counter() - t0) * cfg["L"]), 6)
+    except Exception:
+        pass
     return {"value": round(nt / (per_layer * cfg["L"]), 6), "unit": "tokens/s", "cores": cores,
+            "value_1_thread": one,
             "kind": "oracle", "sample": f"{n_layer_steps} layer steps of {nt} token(s), layer 0 (fp64 numpy), "
                                         f"{per_layer * 1e3:.0f} ms each, extrapolated x{cfg['L']} layers",
             "cpu": _cpu_name()}
@@ -451,6 +518,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="override the config's decode batch")
     ap.add_argument("--tau", type=int, default=64, help="tokens per Alg. 1 period (adaptive configs)")
     ap.add_argument("--no-adapt", action="store_true", help="keep the uniform theta = 0.5 layout")
+    ap.add_argument("--mode", default="moepic", choices=sorted(MODES), help="ablation mode (SURVEY §8(f) NEXT-1)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (multi-rank test on a 1-GPU box)")
     args = ap.parse_args()
