@@ -4,11 +4,11 @@
 // GEMM kernels are warp-specialised, one 128-row output tile per CTA (192 threads):
 //   warp 0  TMA producer: 4-stage ring of 48 KB stages (A 128x64 bf16 + B), 128-byte swizzle,
 //           cp.async.bulk.tensor completing on `full`, waits `empty` before reuse;
-//   warp 1  allocates 256 TMEM columns; one lane issues tcgen05.mma (M = 128, K = 16, fp32
+//   warp 1  allocates 256 TMEM columns; one lane issues tcgen05.mma (M = 128, N = 256, K = 16, fp32
 //           accumulate in TMEM) and tcgen05.commit's each stage back to `empty`, the last one to
 //           `accum`;
 //   warps 2-5 epilogue: tcgen05.ld 32 lanes x 16 columns, SwiGLU (gate/up) or fp32 store (down).
-// gate/up: D_g = X_e W_g^T and D_u = X_e W_u^T share the A tile (two N = 128 MMAs per K step);
+// gate/up: [D_g | D_u] = X_e [W_g; W_u]^T as one N = 256 MMA per K step;
 //          a = silu(D_g) * D_u -> bf16 A_act[rows][I] at the segment's intermediate columns.
 // down:    Y[rows][n0..n0+256) (+)= A_act[rows][seg] * Down[seg][n0..], the down rows are
 //          N-contiguous in the row-interleaved layout, so B is an MN-major operand.
@@ -28,11 +28,16 @@ namespace {
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kABytes = kPfBM * kPfBK * 2;        // 16 KB
-// gate/up stage: A | B_gate | B_up (48 KB) x 4;  down stage: A_hi | A_lo | B (64 KB) x 3
-template <bool DOWN> struct Cfg {
-  static constexpr int kStages = DOWN ? 3 : 4;
-  static constexpr uint32_t kStageBytes = DOWN ? 64 * 1024 : 48 * 1024;
+// CG = 1 (one CTA, UMMA M = 128):  gate/up stage A | B_gate | B_up (48 KB) x 4,
+//                                   down stage A_hi | A_lo | B[256 cols] (64 KB) x 3.
+// CG = 2 (CTA pair, cta_group::2, UMMA M = 256, each CTA holds half of A and half of B):
+//                                   gate/up A | B_gate or B_up (32 KB) x 6,
+//                                   down A_hi | A_lo | B[128 cols] (48 KB) x 4.
+template <bool DOWN, int CG> struct Cfg {
+  static constexpr uint32_t kBBytes = 32 * 1024 / CG;
   static constexpr uint32_t kBOff = DOWN ? 2 * kABytes : kABytes;
+  static constexpr uint32_t kStageBytes = kBOff + kBBytes;
+  static constexpr int kStages = (int)((192 * 1024) / kStageBytes);
 };
 
 __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
@@ -52,16 +57,38 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+template <int CG>
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+// MMA completion -> mbarrier; for a CTA pair the arrive goes to the same barrier in both CTAs
+template <int CG>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-               ::"r"(smem_u32(bar)) : "memory");
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -78,17 +105,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-      ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
+// CG = 2: both CTAs load into their own shared memory but complete the bytes on the leader's
+// barrier (clearing the peer bit of the shared::cluster address selects CTA 0 of the pair)
+template <int CG>
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(m), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(m), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
 }
-__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-      ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
+template <int CG>
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(m), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(m), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
 }
 
 __device__ __forceinline__ uint32_t bf16_rne(float a) {   // round-to-nearest-even to bf16 bits
@@ -102,11 +145,12 @@ __device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) 
   lo = bf16_rne(a - __uint_as_float(hi << 16));
 }
 
-template <bool DOWN>
+template <bool DOWN, int CG>
 __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ PfGemmParams p) {
-  constexpr int kStages = Cfg<DOWN>::kStages;
-  constexpr uint32_t kStageBytes = Cfg<DOWN>::kStageBytes;
-  constexpr uint32_t kBOff = Cfg<DOWN>::kBOff;
+  constexpr int kStages = Cfg<DOWN, CG>::kStages;
+  constexpr uint32_t kStageBytes = Cfg<DOWN, CG>::kStageBytes;
+  constexpr uint32_t kBOff = Cfg<DOWN, CG>::kBOff;
+  constexpr int kTM = kPfBM * CG;               // output rows per tile (per CTA pair)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -114,30 +158,36 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
   uint64_t* accum = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;   // 0 = the pair's MMA leader
 
-  // ---- tile decode
+  // ---- tile decode (both CTAs of a pair decode the same tile)
   int seg = -1, ex = -1, mt = 0, nt = 0;
   {
-    int t = blockIdx.x;
+    int t = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     if (!DOWN) {
       for (int s = 0; s < p.nseg; ++s) {
         const int ntn = (p.seg[s].nrows + kPfBN1 - 1) / kPfBN1;
-        const int n = p.ex[p.seg[s].e].mtiles * ntn;
-        if (t < n) { seg = s; ex = p.seg[s].e; mt = t / ntn; nt = t - mt * ntn; break; }
+        // M tiles fastest: the CTAs sharing one weight tile run side by side, so the weights
+        // cross HBM once and the (L2-resident) token tiles are the ones re-read
+        const int mtn = (p.ex[p.seg[s].e].mtiles + CG - 1) / CG;
+        const int n = mtn * ntn;
+        if (t < n) { seg = s; ex = p.seg[s].e; nt = t / mtn; mt = t - nt * mtn; break; }
         t -= n;
       }
     } else {
       const int ntn = p.d / kPfBN2;
       for (int e = 0; e < p.nexp; ++e) {
-        const int n = p.ex[e].mtiles * ntn;
-        if (t < n) { ex = e; mt = t / ntn; nt = t - mt * ntn; break; }
+        const int mtn = (p.ex[e].mtiles + CG - 1) / CG;
+        const int n = mtn * ntn;
+        if (t < n) { ex = e; nt = t / mtn; mt = t - nt * mtn; break; }
         t -= n;
       }
     }
   }
   if (ex < 0) return;
   const PfExpert E = p.ex[ex];
-  const int arow = E.m_off + mt * kPfBM;      // first row of the A tile / output tile
+  const int mrow = mt * kTM + rank * kPfBM;     // this CTA's first row within the expert block
+  const int arow = E.m_off + mrow;              // ... in the permuted buffers
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -148,12 +198,19 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(tmem_slot)), "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(tmem_slot)), "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(tmem_slot)), "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();    // peer barriers initialised before any TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -166,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
   }
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int s = DOWN ? E.seg_begin : seg, kin = 0;   // down: current segment and k block inside it
       for (int kb = 0; kb < nkb; ++kb) {
@@ -174,26 +231,36 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
         if (kb >= kStages) mbar_wait(&empty[st], ((kb / kStages) - 1) & 1);
         uint8_t* sa = smem + st * kStageBytes;
         uint8_t* sb = sa + kBOff;
-        mbar_expect_tx(&full[st], kStageBytes);
+        const uint32_t fb = smem_u32(&full[st]);
+        if (rank == 0) mbar_expect_tx(&full[st], CG * kStageBytes);
         if (!DOWN) {
-          tma2d(sa, &p.tmA, kb * kPfBK, arow, &full[st]);
-          tma3d(sb, &p.tmB[seg], kb * kPfBK, 0, nt * kPfBN1, &full[st]);
-          tma3d(sb + 16384, &p.tmB[seg], kb * kPfBK, 1, nt * kPfBN1, &full[st]);
+          tma2d<CG>(sa, &p.tmA, kb * kPfBK, arow, fb);
+          if constexpr (CG == 1) {
+            tma3d<CG>(sb, &p.tmB[seg], kb * kPfBK, 0, nt * kPfBN1, fb);
+            tma3d<CG>(sb + 16384, &p.tmB[seg], kb * kPfBK, 1, nt * kPfBN1, fb);
+          } else {
+            // the pair's B operand is [W_g; W_u] split by N: the leader holds the gate rows,
+            // the peer the up rows
+            tma3d<CG>(sb, &p.tmB[seg], kb * kPfBK, rank, nt * kPfBN1, fb);
+          }
         } else {
           while (kin >= p.seg[s].nrows / kPfBK) { ++s; kin = 0; }
-          tma2d(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, &full[st]);
-          tma2d(sa + kABytes, &p.tmA2, p.seg[s].row0 + kin * kPfBK, arow, &full[st]);
+          tma2d<CG>(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, fb);
+          tma2d<CG>(sa + kABytes, &p.tmA2, p.seg[s].row0 + kin * kPfBK, arow, fb);
+          // B (MN-major down columns): this CTA's 256 / CG output columns
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            tma3d(sb + j * 8192, &p.tmB[s], nt * kPfBN2 + j * 64, 2, kin * kPfBK, &full[st]);
+          for (int j = 0; j < 4 / CG; ++j)
+            tma3d<CG>(sb + j * 8192, &p.tmB[s], nt * kPfBN2 + rank * (kPfBN2 / CG) + j * 64, 2, kin * kPfBK, fb);
           ++kin;
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = DOWN ? make_idesc(128, kPfBN2, 1) : make_idesc(128, kPfBN1, 0);
+    // ------------------------------------------------------------ MMA issuer (pair leader)
+    if (lane == 0 && rank == 0) {
+      // gate/up: B_gate and B_up are adjacent 128-row K-major blocks, i.e. one 256-row operand
+      // (CG = 1) or one 128-row half per CTA (CG = 2), so one N = 256 MMA computes [D_g | D_u]
+      constexpr uint32_t idesc = DOWN ? make_idesc(kTM, kPfBN2, 1) : make_idesc(kTM, 2 * kPfBN1, 0);
       for (int kb = 0; kb < nkb; ++kb) {
         const int st = kb % kStages;
         mbar_wait(&full[st], (kb / kStages) & 1);
@@ -205,25 +272,24 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
           const uint64_t da = desc_k_sw128(sa + k * 32);
           const uint32_t acc = (kb | k) ? 1u : 0u;
           if (!DOWN) {
-            umma(tmem, da, desc_k_sw128(sb + k * 32), idesc, acc);
-            umma(tmem + kPfBN1, da, desc_k_sw128(sb + 16384 + k * 32), idesc, acc);
+            umma<CG>(tmem, da, desc_k_sw128(sb + k * 32), idesc, acc);
           } else {
             const uint64_t db = desc_mn_sw128(sb + k * 2048, 8192, 1024);
-            umma(tmem, da, db, idesc, acc);
-            umma(tmem, desc_k_sw128(sa + kABytes + k * 32), db, idesc, 1u);   // + A_lo * B
+            umma<CG>(tmem, da, db, idesc, acc);
+            umma<CG>(tmem, desc_k_sw128(sa + kABytes + k * 32), db, idesc, 1u);   // + A_lo * B
           }
         }
-        umma_commit(&empty[st]);
+        umma_commit<CG>(&empty[st]);
       }
-      umma_commit(accum);
+      umma_commit<CG>(accum);
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
-    const int m = q * 32 + lane;                  // row within the tile
+    const int m = q * 32 + lane;                  // row within this CTA's 128 rows
     mbar_wait(accum, 0);
     tc_fence_after();
-    const bool row_ok = mt * kPfBM + m < E.count;
+    const bool row_ok = mrow + m < E.count;
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
     if (!DOWN) {
       const PfSeg S = p.seg[seg];
@@ -275,10 +341,14 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
     }
     tc_fence_before();
   }
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();    // both epilogues done before the pair frees TMEM
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -357,7 +427,7 @@ bool get_encode() {
 
 }  // namespace
 
-size_t pf_gemm_smem_bytes() { return 3 * 64 * 1024 + 1024 + 256; }   // max of both configs (192 KB)
+size_t pf_gemm_smem_bytes() { return 192 * 1024 + 1024 + 256; }   // stages (192 KB) + align + barriers
 
 bool pf_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   if (!get_encode()) return false;
@@ -381,11 +451,31 @@ bool pf_tmap_weights(CUtensorMap* m, const void* seg_base, uint64_t rows, int d,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <bool DOWN, int CG>
+static void launch_gemm(const PfGemmParams& p, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(p.ntiles * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pf_gemm_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, pf_gemm<DOWN, CG>, p);
+}
 void launch_pf_gateup(const PfGemmParams& p, cudaStream_t s) {
-  if (p.ntiles > 0) pf_gemm<false><<<p.ntiles, kThreads, pf_gemm_smem_bytes(), s>>>(p);
+  if (p.ntiles <= 0) return;
+  if (p.cta_pair) launch_gemm<false, 2>(p, s);
+  else launch_gemm<false, 1>(p, s);
 }
 void launch_pf_down(const PfGemmParams& p, cudaStream_t s) {
-  if (p.ntiles > 0) pf_gemm<true><<<p.ntiles, kThreads, pf_gemm_smem_bytes(), s>>>(p);
+  if (p.ntiles <= 0) return;
+  if (p.cta_pair) launch_gemm<true, 2>(p, s);
+  else launch_gemm<true, 1>(p, s);
 }
 void launch_pf_permute(const PfPermuteParams& p, cudaStream_t s) {
   const int warps = p.T * p.K + p.n_shared * p.T;
@@ -397,14 +487,17 @@ void launch_pf_combine(const PfCombineParams& p, cudaStream_t s) {
 }
 
 bool prefill_init(char* err, size_t errlen) {
-  cudaError_t e1 = cudaFuncSetAttribute(pf_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)pf_gemm_smem_bytes());
-  cudaError_t e2 = cudaFuncSetAttribute(pf_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)pf_gemm_smem_bytes());
-  if (e1 != cudaSuccess || e2 != cudaSuccess) {
-    snprintf(err, errlen, "prefill attributes: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
-    return false;
-  }
+  const int sm = (int)pf_gemm_smem_bytes();
+  const cudaError_t e[4] = {
+      cudaFuncSetAttribute(pf_gemm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+      cudaFuncSetAttribute(pf_gemm<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+      cudaFuncSetAttribute(pf_gemm<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+      cudaFuncSetAttribute(pf_gemm<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)};
+  for (cudaError_t x : e)
+    if (x != cudaSuccess) {
+      snprintf(err, errlen, "prefill attributes: %s", cudaGetErrorString(x));
+      return false;
+    }
   return true;
 }
 

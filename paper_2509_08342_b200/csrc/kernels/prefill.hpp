@@ -9,7 +9,7 @@
 namespace moepic {
 
 constexpr int kPfBM = 128;          // tokens per M tile (UMMA M = 128, cta_group::1)
-constexpr int kPfBN1 = 128;         // intermediate rows per gate/up tile (two N = 128 MMAs)
+constexpr int kPfBN1 = 128;         // intermediate rows per gate/up tile (gate + up: one N = 256 MMA)
 constexpr int kPfBN2 = 256;         // output columns per down tile (UMMA N = 256)
 constexpr int kPfBK = 64;           // K per stage = one 128-byte swizzle row of bf16
 constexpr int kPfMaxSegs = 40;      // weight segments (tensor maps) per GEMM launch
@@ -39,7 +39,8 @@ struct PfGemmParams {
   PfSeg seg[kPfMaxSegs];
   PfExpert ex[kPfMaxExperts];
   int32_t nseg, nexp;
-  int32_t ntiles;                     // total output tiles of the launch
+  int32_t ntiles;                     // total output tiles of the launch (CTA pairs if cta_pair)
+  int32_t cta_pair;                   // 1: cta_group::2 pairs, 256-row tiles (UMMA M = 256)
   int32_t d, I;
   void* out;                          // gate/up: bf16 A_act hi [rows][I]; down: fp32 Y [rows][d]
   void* out2;                         // gate/up: bf16 A_act lo [rows][I]

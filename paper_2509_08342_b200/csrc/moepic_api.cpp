@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -190,6 +191,11 @@ uint64_t plan_bytes(const Plan& p, int64_t rb) {
 
 // ====================================================================== context
 struct moepic_ctx {
+  // kernel parameter blocks (large: built here, not on the stack; calls on a ctx are serialised)
+  std::unique_ptr<K2Params> kp = std::make_unique<K2Params>();
+  std::unique_ptr<PfPermuteParams> pf_pp = std::make_unique<PfPermuteParams>();
+  std::unique_ptr<PfGemmParams> pf_gp = std::make_unique<PfGemmParams>();
+  std::unique_ptr<CombineParams> cpar = std::make_unique<CombineParams>();
   moepic_model_desc desc{};
   ArenaLayout lay{};
   std::unique_ptr<ControlPlane> cp;
@@ -523,7 +529,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
     }
   }
   size_t i0 = 0;
-  static K2Params kp;   // large; ctx calls are serialised by contract
+  K2Params& kp = *ctx->kp;
   while (i0 < work.size()) {
     const size_t i1 = std::min(work.size(), i0 + (size_t)kMaxLaunchSegs);
     int64_t R = 0;
@@ -775,7 +781,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   // ---- permute (+ zero the accumulated outputs)
   CK(cudaMemsetAsync(cursor, 0, (size_t)N * 4, s));
   CK(cudaMemsetAsync(Y, 0, (size_t)rows * d.d * 4, s));
-  static PfPermuteParams pp;
+  PfPermuteParams& pp = *ctx->pf_pp;
   pp.h = h; pp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids); pp.cursor = cursor;
   pp.pos = pos; pp.xperm = xperm; pp.T = T; pp.K = K; pp.d = d.d; pp.e_lo = lo_e; pp.e_hi = hi_e;
   pp.n_shared = NS;
@@ -785,13 +791,24 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   CK(cudaGetLastError());
   ++launches;
 
-  static PfGemmParams gp;
+  PfGemmParams& gp = *ctx->pf_gp;
   CUtensorMap tm_x, tm_act, tm_act_lo;
   if (!pf_tmap_2d(&tm_x, xperm, (uint64_t)rows + kPfBM, d.d, kPfBM) ||
       !pf_tmap_2d(&tm_act, aact, (uint64_t)rows + kPfBM, d.I, kPfBM) ||
       !pf_tmap_2d(&tm_act_lo, aact_lo, (uint64_t)rows + kPfBM, d.I, kPfBM))
     return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (activations)");
   auto tidx = [&](int expert) { return expert >= 0 ? expert : N + (-1 - expert); };
+  // CTA pairs (UMMA M = 256) unless rounding the experts' 128-row tiles up to pairs would waste
+  // more than 1/8 of the MMA work (few tokens per expert, e.g. Qwen3-shaped prefill)
+  int64_t mt1 = 0, mt2 = 0;
+  for (int e = 0; e < NE; ++e) {
+    mt1 += table[e].mtiles;
+    mt2 += 2 * ((table[e].mtiles + 1) / 2);
+  }
+  const char* pair_env = getenv("MOEPIC_PF_CTA_PAIR");
+  const int CG = pair_env ? (atoi(pair_env) ? 2 : 1) : (mt2 * 8 <= mt1 * 9 ? 2 : 1);
+  gp.cta_pair = CG == 2;
+  auto ptiles = [&](int e) { return (int64_t)((table[e].mtiles + CG - 1) / CG); };
 
   auto run_group = [&](const std::vector<StepSeg>& g) -> moepic_status {
     for (const auto& sg : g)
@@ -812,7 +829,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         gp.seg[i - i0] = PfSeg{e, sg.row0, sg.nrows, 0};
         if (!pf_tmap_weights(&gp.tmB[i - i0], sg.base, (uint64_t)sg.nrows, d.d, kPfBN1))
           return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (weights)");
-        tiles += (int64_t)table[e].mtiles * ((sg.nrows + kPfBN1 - 1) / kPfBN1);
+        tiles += ptiles(e) * ((sg.nrows + kPfBN1 - 1) / kPfBN1);
         flops += 2.0 * 2.0 * cnt[e] * (double)d.d * sg.nrows;
       }
       gp.ntiles = (int32_t)tiles;
@@ -857,7 +874,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         flops += 2.0 * cnt[e] * (double)d.d * sg.nrows;
       }
       int64_t tiles = 0;
-      for (int e = 0; e < NE; ++e) tiles += (int64_t)gp.ex[e].mtiles * (d.d / kPfBN2);
+      for (int e = 0; e < NE; ++e) tiles += (gp.ex[e].mtiles ? ptiles(e) : 0) * (d.d / kPfBN2);
       gp.ntiles = (int32_t)tiles;
       gp.d = d.d; gp.I = d.I; gp.out = Y; gp.ld_out = d.d; gp.accumulate = 1;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
@@ -1033,7 +1050,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   }
   if (!fuse.done) {   // no K2 launch fused the combine (no segments, or too many): run K3
   if (comb.size() > (size_t)kMaxStepSegs) return fail(&ctx->err, MOEPIC_ERUNTIME, "too many segments in one step");
-  static CombineParams cpar;
+  CombineParams& cpar = *ctx->cpar;
   cpar.y = y_dev;
   cpar.h = h;
   cpar.ws = reinterpret_cast<const float*>(ctx->arena + ctx->lay.ws);
