@@ -1,13 +1,15 @@
 // Prefill kernels ("experts ... often fully activated"): permute tokens by expert,
 // tcgen05 grouped GEMMs over the split segments, combine.
 //
-// GEMM kernels are warp-specialised, one 128-row output tile per CTA (192 threads):
-//   warp 0  TMA producer: 4-stage ring of 48 KB stages (A 128x64 bf16 + B), 128-byte swizzle,
+// GEMM kernels are persistent and warp-specialised, one CTA (or cta_group::2 CTA pair) per SM,
+// 320 threads:
+//   warp 0  TMA producer: ring of 192 KB of stages (A 128x64 bf16 + B), 128-byte swizzle,
 //           cp.async.bulk.tensor completing on `full`, waits `empty` before reuse;
-//   warp 1  allocates 256 TMEM columns; one lane issues tcgen05.mma (M = 128, N = 256, K = 16, fp32
-//           accumulate in TMEM) and tcgen05.commit's each stage back to `empty`, the last one to
-//           `accum`;
-//   warps 2-5 epilogue: tcgen05.ld 32 lanes x 16 columns, SwiGLU (gate/up) or fp32 store (down).
+//   warp 1  allocates 512 TMEM columns (two 256-column fp32 accumulators); one lane issues
+//           tcgen05.mma (M = 128 or 256 for a pair, N = 256, K = 16) and tcgen05.commit's each
+//           stage back to `empty`, each finished tile to `tfull`;
+//   warps 2-9 epilogue: tcgen05.ld 32 lanes x 16 columns, SwiGLU (gate/up) or fp32 store (down),
+//           then arrive on `tempty` so the MMA warp can reuse that accumulator.
 // gate/up: [D_g | D_u] = X_e [W_g; W_u]^T as one N = 256 MMA per K step;
 //          a = silu(D_g) * D_u -> bf16 A_act[rows][I] at the segment's intermediate columns.
 // down:    Y[rows][n0..n0+256) (+)= A_act[rows][seg] * Down[seg][n0..], the down rows are
@@ -18,6 +20,7 @@
 #include "kernels.hpp"
 #include "device_utils.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -25,8 +28,10 @@ namespace moepic {
 
 namespace {
 
-constexpr int kThreads = 192;
-constexpr uint32_t kTmemCols = 256;
+constexpr int kEpiWarps = 8;                   // 2 per TMEM lane quarter, each half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer warp, MMA warp, epilogue warps
+constexpr uint32_t kAccCols = 256;             // one fp32 accumulator tile (N = 256)
+constexpr uint32_t kTmemCols = 2 * kAccCols;   // double-buffered: epilogue of tile j || MMA of j+1
 constexpr uint32_t kABytes = kPfBM * kPfBK * 2;        // 16 KB
 // CG = 1 (one CTA, UMMA M = 128):  gate/up stage A | B_gate | B_up (48 KB) x 4,
 //                                   down stage A_hi | A_lo | B[256 cols] (64 KB) x 3.
@@ -145,6 +150,43 @@ __device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) 
   lo = bf16_rne(a - __uint_as_float(hi << 16));
 }
 
+// Tile t of a launch -> (segment, expert, m tile, n tile); both CTAs of a pair decode the same
+// tile.  M tiles fastest: the CTAs sharing one weight tile run side by side, so the weights
+// cross HBM once and the (L2-resident) token tiles are the ones re-read.
+template <bool DOWN, int CG>
+__device__ __forceinline__ bool decode_tile(const PfGemmParams& p, int t, int& seg, int& ex, int& mt, int& nt) {
+  if (!DOWN) {
+    for (int s = 0; s < p.nseg; ++s) {
+      const int ntn = (p.seg[s].nrows + kPfBN1 - 1) / kPfBN1;
+      const int mtn = (p.ex[p.seg[s].e].mtiles + CG - 1) / CG;
+      const int n = mtn * ntn;
+      if (t < n) { seg = s; ex = p.seg[s].e; nt = t / mtn; mt = t - nt * mtn; return true; }
+      t -= n;
+    }
+  } else {
+    const int ntn = p.d / kPfBN2;
+    for (int e = 0; e < p.nexp; ++e) {
+      const int mtn = (p.ex[e].mtiles + CG - 1) / CG;
+      const int n = mtn * ntn;
+      if (t < n) { seg = -1; ex = e; nt = t / mtn; mt = t - nt * mtn; return true; }
+      t -= n;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ uint32_t map_to_leader(uint32_t saddr) {   // same offset in CTA 0 of the pair
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Persistent: CTA (pair) c processes tiles c, c + G, c + 2G, ... (G = grid / CG).  The smem
+// ring runs continuously across tiles; the accumulator alternates between two 256-column TMEM
+// buffers so the epilogue of tile j overlaps the main loop of tile j + 1.
 template <bool DOWN, int CG>
 __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ PfGemmParams p) {
   constexpr int kStages = Cfg<DOWN, CG>::kStages;
@@ -155,46 +197,23 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* accum = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* tfull = empty + kStages;            // [2] accumulator ready (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2;                 // [2] accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;   // 0 = the pair's MMA leader
-
-  // ---- tile decode (both CTAs of a pair decode the same tile)
-  int seg = -1, ex = -1, mt = 0, nt = 0;
-  {
-    int t = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-    if (!DOWN) {
-      for (int s = 0; s < p.nseg; ++s) {
-        const int ntn = (p.seg[s].nrows + kPfBN1 - 1) / kPfBN1;
-        // M tiles fastest: the CTAs sharing one weight tile run side by side, so the weights
-        // cross HBM once and the (L2-resident) token tiles are the ones re-read
-        const int mtn = (p.ex[p.seg[s].e].mtiles + CG - 1) / CG;
-        const int n = mtn * ntn;
-        if (t < n) { seg = s; ex = p.seg[s].e; nt = t / mtn; mt = t - nt * mtn; break; }
-        t -= n;
-      }
-    } else {
-      const int ntn = p.d / kPfBN2;
-      for (int e = 0; e < p.nexp; ++e) {
-        const int mtn = (p.ex[e].mtiles + CG - 1) / CG;
-        const int n = mtn * ntn;
-        if (t < n) { ex = e; nt = t / mtn; mt = t - nt * mtn; break; }
-        t -= n;
-      }
-    }
-  }
-  if (ex < 0) return;
-  const PfExpert E = p.ex[ex];
-  const int mrow = mt * kTM + rank * kPfBM;     // this CTA's first row within the expert block
-  const int arow = E.m_off + mrow;              // ... in the permuted buffers
+  const int G = (int)gridDim.x / CG;
+  const int c0 = (int)blockIdx.x / CG;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(accum, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps * CG);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -214,44 +233,52 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // number of K blocks
-  int nkb;
-  if (!DOWN) nkb = p.d / kPfBK;
-  else {
-    nkb = 0;
-    for (int s = E.seg_begin; s < E.seg_end; ++s) nkb += p.seg[s].nrows / kPfBK;
-  }
+  auto nkb_of = [&](int ex) {
+    if (!DOWN) return p.d / kPfBK;
+    const PfExpert& E = p.ex[ex];
+    int n = 0;
+    for (int s = E.seg_begin; s < E.seg_end; ++s) n += p.seg[s].nrows / kPfBK;
+    return n;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
-      int s = DOWN ? E.seg_begin : seg, kin = 0;   // down: current segment and k block inside it
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % kStages;
-        if (kb >= kStages) mbar_wait(&empty[st], ((kb / kStages) - 1) & 1);
-        uint8_t* sa = smem + st * kStageBytes;
-        uint8_t* sb = sa + kBOff;
-        const uint32_t fb = smem_u32(&full[st]);
-        if (rank == 0) mbar_expect_tx(&full[st], CG * kStageBytes);
-        if (!DOWN) {
-          tma2d<CG>(sa, &p.tmA, kb * kPfBK, arow, fb);
-          if constexpr (CG == 1) {
-            tma3d<CG>(sb, &p.tmB[seg], kb * kPfBK, 0, nt * kPfBN1, fb);
-            tma3d<CG>(sb + 16384, &p.tmB[seg], kb * kPfBK, 1, nt * kPfBN1, fb);
+      int it = 0;                                // k blocks issued so far (ring position)
+      for (int t = c0; t < p.ntiles; t += G) {
+        int seg, ex, mt, nt;
+        decode_tile<DOWN, CG>(p, t, seg, ex, mt, nt);
+        const PfExpert& E = p.ex[ex];
+        const int arow = E.m_off + mt * kTM + rank * kPfBM;
+        const int nkb = nkb_of(ex);
+        int s = DOWN ? E.seg_begin : seg, kin = 0;   // down: current segment and k block inside it
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+          uint8_t* sa = smem + st * kStageBytes;
+          uint8_t* sb = sa + kBOff;
+          const uint32_t fb = smem_u32(&full[st]);
+          if (rank == 0) mbar_expect_tx(&full[st], CG * kStageBytes);
+          if (!DOWN) {
+            tma2d<CG>(sa, &p.tmA, kb * kPfBK, arow, fb);
+            if constexpr (CG == 1) {
+              tma3d<CG>(sb, &p.tmB[seg], kb * kPfBK, 0, nt * kPfBN1, fb);
+              tma3d<CG>(sb + 16384, &p.tmB[seg], kb * kPfBK, 1, nt * kPfBN1, fb);
+            } else {
+              // the pair's B operand is [W_g; W_u] split by N: the leader holds the gate rows,
+              // the peer the up rows
+              tma3d<CG>(sb, &p.tmB[seg], kb * kPfBK, rank, nt * kPfBN1, fb);
+            }
           } else {
-            // the pair's B operand is [W_g; W_u] split by N: the leader holds the gate rows,
-            // the peer the up rows
-            tma3d<CG>(sb, &p.tmB[seg], kb * kPfBK, rank, nt * kPfBN1, fb);
-          }
-        } else {
-          while (kin >= p.seg[s].nrows / kPfBK) { ++s; kin = 0; }
-          tma2d<CG>(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, fb);
-          tma2d<CG>(sa + kABytes, &p.tmA2, p.seg[s].row0 + kin * kPfBK, arow, fb);
-          // B (MN-major down columns): this CTA's 256 / CG output columns
+            while (kin >= p.seg[s].nrows / kPfBK) { ++s; kin = 0; }
+            tma2d<CG>(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, fb);
+            tma2d<CG>(sa + kABytes, &p.tmA2, p.seg[s].row0 + kin * kPfBK, arow, fb);
+            // B (MN-major down columns): this CTA's 256 / CG output columns
 #pragma unroll
-          for (int j = 0; j < 4 / CG; ++j)
-            tma3d<CG>(sb + j * 8192, &p.tmB[s], nt * kPfBN2 + rank * (kPfBN2 / CG) + j * 64, 2, kin * kPfBK, fb);
-          ++kin;
+            for (int j = 0; j < 4 / CG; ++j)
+              tma3d<CG>(sb + j * 8192, &p.tmB[s], nt * kPfBN2 + rank * (kPfBN2 / CG) + j * 64, 2, kin * kPfBK, fb);
+            ++kin;
+          }
         }
       }
     }
@@ -261,87 +288,112 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
       // gate/up: B_gate and B_up are adjacent 128-row K-major blocks, i.e. one 256-row operand
       // (CG = 1) or one 128-row half per CTA (CG = 2), so one N = 256 MMA computes [D_g | D_u]
       constexpr uint32_t idesc = DOWN ? make_idesc(kTM, kPfBN2, 1) : make_idesc(kTM, 2 * kPfBN1, 0);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % kStages;
-        mbar_wait(&full[st], (kb / kStages) & 1);
+      int it = 0, j = 0;
+      for (int t = c0; t < p.ntiles; t += G, ++j) {
+        int seg, ex, mt, nt;
+        decode_tile<DOWN, CG>(p, t, seg, ex, mt, nt);
+        const int nkb = nkb_of(ex);
+        const int acc_buf = j & 1;
+        if (j >= 2) mbar_wait(&tempty[acc_buf], ((j >> 1) - 1) & 1);   // epilogue drained it
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + st * kStageBytes);
-        const uint32_t sb = sa + kBOff;
+        const uint32_t d = tmem + (uint32_t)acc_buf * kAccCols;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * kStageBytes);
+          const uint32_t sb = sa + kBOff;
 #pragma unroll
-        for (int k = 0; k < kPfBK / 16; ++k) {
-          const uint64_t da = desc_k_sw128(sa + k * 32);
-          const uint32_t acc = (kb | k) ? 1u : 0u;
-          if (!DOWN) {
-            umma<CG>(tmem, da, desc_k_sw128(sb + k * 32), idesc, acc);
-          } else {
-            const uint64_t db = desc_mn_sw128(sb + k * 2048, 8192, 1024);
-            umma<CG>(tmem, da, db, idesc, acc);
-            umma<CG>(tmem, desc_k_sw128(sa + kABytes + k * 32), db, idesc, 1u);   // + A_lo * B
+          for (int k = 0; k < kPfBK / 16; ++k) {
+            const uint64_t da = desc_k_sw128(sa + k * 32);
+            const uint32_t acc = (kb | k) ? 1u : 0u;
+            if (!DOWN) {
+              umma<CG>(d, da, desc_k_sw128(sb + k * 32), idesc, acc);
+            } else {
+              const uint64_t db = desc_mn_sw128(sb + k * 2048, 8192, 1024);
+              umma<CG>(d, da, db, idesc, acc);
+              umma<CG>(d, desc_k_sw128(sa + kABytes + k * 32), db, idesc, 1u);   // + A_lo * B
+            }
           }
+          umma_commit<CG>(&empty[st]);
         }
-        umma_commit<CG>(&empty[st]);
+        umma_commit<CG>(&tfull[acc_buf]);
       }
-      umma_commit<CG>(accum);
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------------------ epilogue (warps 2..9)
+    const int ew = warp - 2;
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
+    const int half = ew >> 2;                     // which half of the tile's columns
     const int m = q * 32 + lane;                  // row within this CTA's 128 rows
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    const bool row_ok = mrow + m < E.count;
-    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
-    if (!DOWN) {
-      const PfSeg S = p.seg[seg];
-      const size_t off = (size_t)(arow + m) * p.ld_out + S.row0 + nt * kPfBN1;
-      uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + off;
-      uint16_t* out_lo = reinterpret_cast<uint16_t*>(p.out2) + off;
-      for (int c = 0; c < kPfBN1; c += 16) {
-        float g[16], u[16];
-        tmem_ld16(tbase + c, g);
-        tmem_ld16(tbase + kPfBN1 + c, u);
-        if (row_ok && nt * kPfBN1 + c < S.nrows) {
-          uint32_t ph[8], pl[8];
+    const uint32_t tempty_addr0 = CG == 2 ? map_to_leader(smem_u32(&tempty[0])) : smem_u32(&tempty[0]);
+    int j = 0;
+    for (int t = c0; t < p.ntiles; t += G, ++j) {
+      int seg, ex, mt, nt;
+      decode_tile<DOWN, CG>(p, t, seg, ex, mt, nt);
+      const PfExpert& E = p.ex[ex];
+      const int mrow = mt * kTM + rank * kPfBM;
+      const int arow = E.m_off + mrow;
+      const int acc_buf = j & 1;
+      mbar_wait(&tfull[acc_buf], (j >> 1) & 1);
+      tc_fence_after();
+      const bool row_ok = mrow + m < E.count;
+      const uint32_t tbase = tmem + (uint32_t)acc_buf * kAccCols + ((uint32_t)(q * 32) << 16);
+      if (!DOWN) {
+        const PfSeg S = p.seg[seg];
+        const size_t off = (size_t)(arow + m) * p.ld_out + S.row0 + nt * kPfBN1;
+        uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + off;
+        uint16_t* out_lo = reinterpret_cast<uint16_t*>(p.out2) + off;
+        for (int c = half * (kPfBN1 / 2); c < (half + 1) * (kPfBN1 / 2); c += 16) {
+          float g[16], u[16];
+          tmem_ld16(tbase + c, g);
+          tmem_ld16(tbase + kPfBN1 + c, u);
+          if (row_ok && nt * kPfBN1 + c < S.nrows) {
+            uint32_t ph[8], pl[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
-            const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
-            uint32_t h0, l0, h1, l1;
-            split_bf16(a0, h0, l0);
-            split_bf16(a1, h1, l1);
-            ph[i] = h0 | (h1 << 16);
-            pl[i] = l0 | (l1 << 16);
-          }
-          uint4* o = reinterpret_cast<uint4*>(out + c);
-          o[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-          o[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
-          uint4* ol = reinterpret_cast<uint4*>(out_lo + c);
-          ol[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-          ol[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
-        }
-      }
-    } else {
-      float* out = reinterpret_cast<float*>(p.out) + (size_t)(arow + m) * p.ld_out + nt * kPfBN2;
-      for (int c = 0; c < kPfBN2; c += 16) {
-        float v[16];
-        tmem_ld16(tbase + c, v);
-        if (row_ok) {
-          float4* o = reinterpret_cast<float4*>(out + c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            if (p.accumulate) {
-              const float4 y = o[i];
-              x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+            for (int i = 0; i < 8; ++i) {
+              const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
+              const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
+              uint32_t h0, l0, h1, l1;
+              split_bf16(a0, h0, l0);
+              split_bf16(a1, h1, l1);
+              ph[i] = h0 | (h1 << 16);
+              pl[i] = l0 | (l1 << 16);
             }
-            o[i] = x;
+            uint4* o = reinterpret_cast<uint4*>(out + c);
+            o[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+            o[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
+            uint4* ol = reinterpret_cast<uint4*>(out_lo + c);
+            ol[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+            ol[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
+          }
+        }
+      } else {
+        float* out = reinterpret_cast<float*>(p.out) + (size_t)(arow + m) * p.ld_out + nt * kPfBN2;
+        for (int c = half * (kPfBN2 / 2); c < (half + 1) * (kPfBN2 / 2); c += 16) {
+          float v[16];
+          tmem_ld16(tbase + c, v);
+          if (row_ok) {
+            float4* o = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              if (p.accumulate) {
+                const float4 y = o[i];
+                x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+              }
+              o[i] = x;
+            }
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_addr0 + (uint32_t)acc_buf * 8);   // the leader's barrier
     }
-    tc_fence_before();
   }
-  if constexpr (CG == 2) cluster_sync_all();    // both epilogues done before the pair frees TMEM
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync_all();    // both CTAs done before the pair frees TMEM
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -427,7 +479,7 @@ bool get_encode() {
 
 }  // namespace
 
-size_t pf_gemm_smem_bytes() { return 192 * 1024 + 1024 + 256; }   // stages (192 KB) + align + barriers
+size_t pf_gemm_smem_bytes() { return 192 * 1024 + 1024 + 512; }   // stages (192 KB) + align + barriers
 
 bool pf_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   if (!get_encode()) return false;
@@ -454,7 +506,10 @@ bool pf_tmap_weights(CUtensorMap* m, const void* seg_base, uint64_t rows, int d,
 template <bool DOWN, int CG>
 static void launch_gemm(const PfGemmParams& p, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(p.ntiles * CG));
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ctas = std::min(p.ntiles, sms / CG) * CG;   // persistent: one CTA (pair) per SM (pair)
+  cfg.gridDim = dim3((unsigned)ctas);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pf_gemm_smem_bytes();
   cfg.stream = s;
