@@ -37,7 +37,13 @@ struct RouterParams {
   unsigned long long* mb_rank;
   uint32_t seq;
   int B, d, N, K, renorm;
+  // batches above kRouterSplitB: phase 1 only in k1_router, selection in k1_select (one warp per
+  // token, per-expert prediction count / max logit reduced with atomics into sel_cnt / sel_max)
+  unsigned int* ticket2;            // zero-initialised, reset by k1_select
+  int32_t* sel_cnt;                 // [N] zero-initialised, reset by k1_select
+  unsigned long long* sel_max;      // [N] order-preserving max-logit keys, reset to 0
 };
+constexpr int kRouterSplitB = 32;
 void launch_router(const RouterParams& p, cudaStream_t s);
 
 // ------------------------------------------------------------------ K2: split-expert stream

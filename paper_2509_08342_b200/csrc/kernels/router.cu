@@ -8,6 +8,8 @@
 // mapped-pinned mailbox, system fence, then `seq_route` — the host starts planning copies now.
 // Phase 3 (same CTA): batch ranking of the next layer's experts (reading Q9) by warp ballots
 // (rank_j = #experts whose key precedes j's), published with `seq_rank`.
+// Batches above kRouterSplitB (prefill) run phases 2-3 in k1_select instead: one warp per token,
+// so the selection is spread over the whole GPU rather than one CTA.
 #include "kernels.hpp"
 #include "device_utils.cuh"
 
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
       if (lane == 0) p.logits[(size_t)m * BN + rem] = acc;
     }
   }
+  if (p.B > kRouterSplitB) return;   // large batch: k1_select does phases 2 and 3
   // ---- the last CTA to finish phase 1 does the selection
   __threadfence();
   __syncthreads();
@@ -167,10 +170,118 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
   if (threadIdx.x == 0) *p.ticket = 0u;
 }
 
+// order-preserving map double -> u64 (larger double <-> larger key; 0 is below every logit)
+__device__ __forceinline__ unsigned long long order_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double order_val(unsigned long long k) {
+  return __longlong_as_double((long long)((k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+}
+
+// Large-batch selection (prefill): one warp per token for the routing top-K / Eq. 2 weights and
+// the predicted top-K (Eq. 3 counts and max logits, reading Q9); the last CTA ranks the next
+// layer's experts.  Same keys and arithmetic as phases 2-3 of k1_router.
+__global__ void __launch_bounds__(256) k1_select(RouterParams p) {
+  __shared__ int s_last;
+  __shared__ int s_topk[8][64];
+  __shared__ int s_cnt[kMaxN];
+  __shared__ unsigned long long s_max[kMaxN];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int BN = p.B * p.N;
+  const double* L0 = p.logits;
+  const double* L1 = p.logits + BN;
+  const unsigned long long tag = (unsigned long long)p.seq << 32;
+  const int b = blockIdx.x * 8 + warp;
+  for (int j = threadIdx.x; j < p.N; j += blockDim.x) {
+    s_cnt[j] = 0;
+    s_max[j] = 0ull;
+  }
+  __syncthreads();
+  if (b < p.B) {
+    if (p.W0 != nullptr) {
+      unsigned bits;
+      const double* row = L0 + (size_t)b * p.N;
+      warp_topk(row, p.N, p.K, s_topk[warp], &bits);
+      __syncwarp();
+      const double mx = row[s_topk[warp][0]];
+      double ek = 0.0, part = 0.0;
+      if (lane < p.K) ek = exp(row[s_topk[warp][lane]] - mx);
+      if (p.renorm) {
+        part = ek;
+      } else {
+        for (int j = lane; j < p.N; j += 32) part += exp(row[j] - mx);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane < p.K) {
+        const int id = s_topk[warp][lane];
+        const float wv = (float)(ek / part);
+        p.ids[b * p.K + lane] = id;
+        p.w[b * p.K + lane] = wv;
+        p.mb_ids[b * p.K + lane] = tag | (uint32_t)id;
+        p.mb_w[b * p.K + lane] = tag | __float_as_uint(wv);
+      }
+      __syncwarp();
+    }
+    if (p.W1 != nullptr) {
+      unsigned bits;
+      const double* row = L1 + (size_t)b * p.N;
+      warp_topk(row, p.N, p.K, s_topk[warp], &bits);
+      for (int q = 0, j = lane; j < p.N; ++q, j += 32) {
+        if (bits & (1u << q)) atomicAdd(&s_cnt[j], 1);
+        atomicMax(&s_max[j], order_key(row[j]));
+      }
+    }
+  }
+  if (p.W1 == nullptr) return;
+  __syncthreads();
+  for (int j = threadIdx.x; j < p.N; j += blockDim.x) {   // one global atomic per expert per CTA
+    if (s_cnt[j]) atomicAdd(&p.sel_cnt[j], s_cnt[j]);
+    if (s_max[j]) atomicMax(&p.sel_max[j], s_max[j]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(p.ticket2, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ranking: key = (count desc, max logit desc, id asc)
+  const int nwarps = blockDim.x >> 5;
+  for (int j = warp; j < p.N; j += nwarps) {
+    const int cj = *((volatile int*)&p.sel_cnt[j]);
+    const double mj = order_val(*((volatile unsigned long long*)&p.sel_max[j]));
+    int r = 0;
+    for (int o0 = 0; o0 < p.N; o0 += 32) {
+      const int o = o0 + lane;
+      bool before = false;
+      if (o < p.N) {
+        const int co = *((volatile int*)&p.sel_cnt[o]);
+        const double mo = order_val(*((volatile unsigned long long*)&p.sel_max[o]));
+        before = (co > cj) || (co == cj && (mo > mj || (mo == mj && o < j)));
+      }
+      r += __popc(__ballot_sync(0xffffffffu, before));
+    }
+    if (lane == 0) p.ranking[r] = j;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < p.N; i += blockDim.x) {
+    p.mb_rank[i] = tag | (uint32_t)p.ranking[i];
+    p.sel_cnt[i] = 0;
+    p.sel_max[i] = 0ull;
+  }
+  if (threadIdx.x == 0) *p.ticket2 = 0u;
+}
+
 void launch_router(const RouterParams& p, cudaStream_t s) {
   const int warps = 2 * p.B * p.N;
   const int grid = (warps + 7) / 8;
   k1_router<<<grid, 256, 0, s>>>(p);
+  if (p.B > kRouterSplitB) k1_select<<<(p.B + 7) / 8, 256, 0, s>>>(p);
 }
 
 }  // namespace moepic

@@ -37,7 +37,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
-  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, total;
+  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, total;
   uint64_t pool_rows, plan_rows, od_rows, ws_floats;
   // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
   size_t xperm, aact, yperm, pos, cursor;
@@ -88,6 +88,7 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   a.w = off; off = align_up(off + (size_t)d.max_batch * d.K * 4);
   a.ranking = off; off = align_up(off + (size_t)d.N * 4);
   a.ticket = off; off = align_up(off + 64);
+  a.rsel = off; off = align_up(off + (size_t)d.N * 16);   // k1_select: cnt int32 [N] | max u64 [N]
   a.pf_rows = 0;
   a.xperm = a.aact = a.yperm = a.pos = a.cursor = off;
   if (d.max_batch > kDecodeMaxB) {
@@ -395,7 +396,9 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
   for (auto& e : ctx->feed_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
-  if (cudaMemset(ctx->arena + lay.ticket, 0, 64) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
+  if (cudaMemset(ctx->arena + lay.ticket, 0, 64) != cudaSuccess ||
+      cudaMemset(ctx->arena + lay.rsel, 0, (size_t)desc->N * 16) != cudaSuccess)
+    return bail(MOEPIC_ERUNTIME);
   ctx->slot_base.assign(desc->L, 0);
   ctx->ids_h.resize((size_t)desc->max_batch * desc->K);
   ctx->w_h.resize((size_t)desc->max_batch * desc->K);
@@ -659,6 +662,9 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   rp.w = reinterpret_cast<float*>(ctx->arena + ctx->lay.w);
   rp.ranking = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.ranking);
   rp.ticket = reinterpret_cast<unsigned int*>(ctx->arena + ctx->lay.ticket);
+  rp.ticket2 = reinterpret_cast<unsigned int*>(ctx->arena + ctx->lay.ticket + 16);
+  rp.sel_cnt = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.rsel);
+  rp.sel_max = reinterpret_cast<unsigned long long*>(ctx->arena + ctx->lay.rsel + (size_t)d.N * 8);
   uint8_t* mb = ctx->mailbox_dev;
   const size_t BK = (size_t)d.max_batch * d.K;
   rp.mb_ids = reinterpret_cast<unsigned long long*>(mb + 64);
@@ -670,7 +676,7 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   launch_router(rp, s);
   ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
   CK(cudaGetLastError());
-  ctx->ctr.kernel_launches++;
+  ctx->ctr.kernel_launches += B > kRouterSplitB ? 2 : 1;
   if (read_ids) {
     const size_t n = (size_t)B * d.K;
     moepic_status st = wait_mailbox(ctx, s, 0, n);
@@ -798,17 +804,19 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
       !pf_tmap_2d(&tm_act_lo, aact_lo, (uint64_t)rows + kPfBM, d.I, kPfBM))
     return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (activations)");
   auto tidx = [&](int expert) { return expert >= 0 ? expert : N + (-1 - expert); };
-  // CTA pairs (UMMA M = 256) unless rounding the experts' 128-row tiles up to pairs would waste
-  // more than 1/8 of the MMA work (few tokens per expert, e.g. Qwen3-shaped prefill)
+  // gate/up runs on CTA pairs (UMMA M = 256: half the B operand bytes per SM; ncu: tensor pipe
+  // 88% vs 75% for single CTAs) unless rounding the experts' 128-row tiles up to pairs would
+  // waste more than 1/10 of the MMA work (few tokens per expert, e.g. Qwen3-shaped prefill).
+  // down keeps single CTAs (90% vs 84%: its B tile is already shared by both MMAs, hi and lo).
   int64_t mt1 = 0, mt2 = 0;
   for (int e = 0; e < NE; ++e) {
     mt1 += table[e].mtiles;
     mt2 += 2 * ((table[e].mtiles + 1) / 2);
   }
-  const char* pair_env = getenv("MOEPIC_PF_CTA_PAIR");
-  const int CG = pair_env ? (atoi(pair_env) ? 2 : 1) : (mt2 * 8 <= mt1 * 9 ? 2 : 1);
-  gp.cta_pair = CG == 2;
-  auto ptiles = [&](int e) { return (int64_t)((table[e].mtiles + CG - 1) / CG); };
+  const char* pair_env = getenv("MOEPIC_PF_CTA_PAIR");   // 0 / 1 forces both GEMMs (tests)
+  const int CGu = pair_env ? (atoi(pair_env) ? 2 : 1) : (mt2 * 10 <= mt1 * 11 ? 2 : 1);
+  const int CGd = pair_env ? (atoi(pair_env) ? 2 : 1) : 1;
+  auto ptiles = [&](int e, int CG) { return (int64_t)((table[e].mtiles + CG - 1) / CG); };
 
   auto run_group = [&](const std::vector<StepSeg>& g) -> moepic_status {
     for (const auto& sg : g)
@@ -829,10 +837,11 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         gp.seg[i - i0] = PfSeg{e, sg.row0, sg.nrows, 0};
         if (!pf_tmap_weights(&gp.tmB[i - i0], sg.base, (uint64_t)sg.nrows, d.d, kPfBN1))
           return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (weights)");
-        tiles += ptiles(e) * ((sg.nrows + kPfBN1 - 1) / kPfBN1);
+        tiles += ptiles(e, CGu) * ((sg.nrows + kPfBN1 - 1) / kPfBN1);
         flops += 2.0 * 2.0 * cnt[e] * (double)d.d * sg.nrows;
       }
       gp.ntiles = (int32_t)tiles;
+      gp.cta_pair = CGu == 2;
       gp.d = d.d; gp.I = d.I; gp.out = aact; gp.out2 = aact_lo; gp.ld_out = d.I; gp.accumulate = 0;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
       launch_pf_gateup(gp, s);
@@ -874,8 +883,9 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         flops += 2.0 * cnt[e] * (double)d.d * sg.nrows;
       }
       int64_t tiles = 0;
-      for (int e = 0; e < NE; ++e) tiles += (gp.ex[e].mtiles ? ptiles(e) : 0) * (d.d / kPfBN2);
+      for (int e = 0; e < NE; ++e) tiles += (gp.ex[e].mtiles ? ptiles(e, CGd) : 0) * (d.d / kPfBN2);
       gp.ntiles = (int32_t)tiles;
+      gp.cta_pair = CGd == 2;
       gp.d = d.d; gp.I = d.I; gp.out = Y; gp.ld_out = d.d; gp.accumulate = 1;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
       launch_pf_down(gp, s);
