@@ -12,7 +12,7 @@ constexpr int kPfBM = 128;          // tokens per M tile (UMMA M = 128, cta_grou
 constexpr int kPfBN1 = 128;         // intermediate rows per gate/up tile (gate + up: one N = 256 MMA)
 constexpr int kPfBN2 = 256;         // output columns per down tile (UMMA N = 256)
 constexpr int kPfBK = 64;           // K per stage = one 128-byte swizzle row of bf16
-constexpr int kPfMaxSegs = 40;      // weight segments (tensor maps) per GEMM launch
+constexpr int kPfMaxSegs = 136;     // weight segments (tensor maps) per GEMM launch (params ~24 KB)
 constexpr int kPfMaxExperts = 136;  // experts (incl. shared) per launch
 
 // One weight segment: rows [row0, row0 + nrows) of expert `e` (row0 = its first intermediate
