@@ -268,7 +268,7 @@ def run_ours(args, log):
     if dist:
         dist.barrier()
     c0 = ctx.counters()
-    ctx.profile(True)
+    ctx.profile(not args.no_kernel_events)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
@@ -519,6 +519,8 @@ def main():
     ap.add_argument("--tau", type=int, default=64, help="tokens per Alg. 1 period (adaptive configs)")
     ap.add_argument("--no-adapt", action="store_true", help="keep the uniform theta = 0.5 layout")
     ap.add_argument("--mode", default="moepic", choices=sorted(MODES), help="ablation mode (SURVEY §8(f) NEXT-1)")
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="time the step without the per-kernel CUDA events (roofline fields then empty)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (multi-rank test on a 1-GPU box)")
     args = ap.parse_args()

@@ -1,0 +1,77 @@
+// Combine of the step's partials, shared by the fused tail of the
+// final K2 launch and by the stand-alone K3.
+//
+// y[b][c] = (h[b][c] if residual) + sum over the partial vectors serving token b.  The partials
+// of token b are enumerated in a fixed order (segments in step order, chunks in CTA order) and
+// numbered k = 0, 1, ...; warp w of the 16 sums the k = w (mod 16) ones in increasing k with its
+// lanes on 32 consecutive float4 columns (coalesced), and the 16 warp sums are added in warp
+// order.  The order depends only on the step's segment table, so the result is deterministic
+// and identical for the fused and the stand-alone combine.
+#pragma once
+
+#include "kernels.hpp"
+#include "device_utils.cuh"
+
+namespace moepic {
+
+constexpr int kCombineWarps = 16;
+
+// Column block `blk` of B * ceil(d / 128): token b = blk / ncb, float4 columns [32 cb, 32 cb + 32).
+// Must be called by all kCombineWarps * 32 threads of the block; `red` is 16 * 32 float4 of smem.
+__device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, int nsegs, const float* ws,
+                                              const uint16_t* h, float* y, int d, int residual,
+                                              float4* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d4 = d >> 2;
+  const int ncb = (d4 + 31) >> 5;
+  const int b = blk / ncb;
+  const int c4 = (blk - b * ncb) * 32 + lane;
+  const bool active = c4 < d4;
+  const uint32_t bit = 1u << b;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k0 = 0;   // index of the first chunk of the current segment in token b's list
+  for (int s = 0; s < nsegs; ++s) {
+    const CombineSeg sg = segs[s];
+    if (!(sg.tok_mask & bit)) continue;
+    const int ntok = __popc(sg.tok_mask);
+    const int t = __popc(sg.tok_mask & (bit - 1u));
+    const int64_t stride4 = (int64_t)ntok * d4;
+    const float4* base = reinterpret_cast<const float4*>(ws + sg.ws_off + (int64_t)t * d) + c4;
+    int ci = (warp - k0) & (kCombineWarps - 1);   // first chunk with k = w (mod 16)
+    if (active) {
+      for (; ci + 3 * kCombineWarps < sg.nchunks; ci += 4 * kCombineWarps) {   // 4 loads in flight
+        const float4 v0 = base[(int64_t)ci * stride4];
+        const float4 v1 = base[(int64_t)(ci + kCombineWarps) * stride4];
+        const float4 v2 = base[(int64_t)(ci + 2 * kCombineWarps) * stride4];
+        const float4 v3 = base[(int64_t)(ci + 3 * kCombineWarps) * stride4];
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+      }
+      for (; ci < sg.nchunks; ci += kCombineWarps) {
+        const float4 v = base[(int64_t)ci * stride4];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    }
+    k0 += sg.nchunks;
+  }
+  red[warp * 32 + lane] = acc;
+  __syncthreads();
+  if (warp == 0 && active) {
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (residual) {
+      const uint2 hv = reinterpret_cast<const uint2*>(h + (size_t)b * d)[c4];
+      r = make_float4(bf16lo(hv.x), bf16hi(hv.x), bf16lo(hv.y), bf16hi(hv.y));
+    }
+#pragma unroll
+    for (int w = 0; w < kCombineWarps; ++w) {
+      const float4 v = red[w * 32 + lane];
+      r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
+    }
+    reinterpret_cast<float4*>(y + (size_t)b * d)[c4] = r;
+  }
+  __syncthreads();   // `red` is reused by the next block
+}
+
+}  // namespace moepic

@@ -22,6 +22,7 @@
 // cores are for prefill.
 #include "kernels.hpp"
 #include "device_utils.cuh"
+#include "combine_dev.cuh"
 
 #include <cstdio>
 
@@ -341,42 +342,12 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       __threadfence();
     }
     __syncthreads();
-    // CTA c adds items [c W / G, (c+1) W / G) of the B x d/4 float4 outputs; each item sums its
-    // segments' per-CTA partials in K3's order (8 interleaved accumulators, then in order)
-    const int d4 = d >> 2;
-    const int64_t W = (int64_t)p.B * d4;
-    const int64_t lo = (int64_t)blockIdx.x * W / G, hi = (int64_t)(blockIdx.x + 1) * W / G;
-    for (int64_t q = lo + tid; q < hi; q += kThreads) {
-      const int b = (int)(q / d4);
-      const int c4 = (int)(q - (int64_t)b * d4);
-      const uint32_t bit = 1u << b;
-      float4 acc[8];
-#pragma unroll
-      for (int w2 = 0; w2 < 8; ++w2) acc[w2] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s = 0; s < p.ncomb; ++s) {
-        const CombineSeg sg = p.comb[s];
-        if (!(sg.tok_mask & bit)) continue;
-        const int ntok = __popc(sg.tok_mask);
-        const int t = __popc(sg.tok_mask & (bit - 1u));
-        const float4* base = reinterpret_cast<const float4*>(p.ws + sg.ws_off + (int64_t)t * d) + c4;
-        const int64_t stride4 = (int64_t)ntok * d4;
-        for (int ci = 0; ci < sg.nchunks; ++ci) {
-          const float4 v = base[(int64_t)ci * stride4];
-          float4& a = acc[ci & 7];
-          a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-        }
-      }
-      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (p.residual) {
-        const uint2 hv = reinterpret_cast<const uint2*>(p.h + (size_t)b * d)[c4];
-        r = make_float4(bf16lo(hv.x), bf16hi(hv.x), bf16lo(hv.y), bf16hi(hv.y));
-      }
-#pragma unroll
-      for (int w2 = 0; w2 < 8; ++w2) {
-        r.x += acc[w2].x; r.y += acc[w2].y; r.z += acc[w2].z; r.w += acc[w2].w;
-      }
-      reinterpret_cast<float4*>(p.y + (size_t)b * d)[c4] = r;
-    }
+    // CTA c combines column blocks c, c + G, ... (combine_dev.cuh: 16 warps over the partials,
+    // lanes over 32 float4 columns, fixed order); the K2 smem ring is free again here
+    float4* red = reinterpret_cast<float4*>(smem);
+    const int nblk = p.B * ((((d >> 2)) + 31) >> 5);
+    for (int blk = blockIdx.x; blk < nblk; blk += G)
+      combine_block(blk, p.comb, p.ncomb, p.ws, p.h, p.y, d, p.residual, red);
   }
 }
 
