@@ -354,8 +354,17 @@ def run_ours(args, log):
                 "flops_per_launch": int(kg["bytes"] / max(1, kg["launches"])),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
     else:
+        traffic, tsrc = None, None
+        try:   # ncu --set full DRAM bytes of a captured K2 launch of this shape (scripts/ncu_traffic.py)
+            ent = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[cfg["shape"]]
+            if k2["launches"] and "ratio" in ent:
+                traffic = int(ent["ratio"] * k2["bytes"] / k2["launches"])
+                tsrc = {k: ent[k] for k in ("dram_bytes_per_launch", "alg_bytes_per_launch", "ratio", "report")}
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": "k2_split_expert", "achieved": round(k2_gbs, 1),
-                "peak": hbm_peak, "unit": "GB/s", "frac": round(k2_gbs / hbm_peak, 4), "traffic": None,
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(k2_gbs / hbm_peak, 4), "traffic": traffic,
+                "traffic_source": tsrc,
                 "launches": k2["launches"], "avg_launch_us": round(k2["total_ms"] * 1e3 / max(1, k2["launches"]), 2),
                 "bytes_per_launch": int(k2["bytes"] / max(1, k2["launches"])),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"}

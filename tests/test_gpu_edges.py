@@ -101,3 +101,17 @@ def test_configure_drops_pending_prefetch():
     ctx.configure(**cfg2)
     orc.configure(CacheConfig(**cfg2))
     _run(m, ctx, orc, H[1:], 1, 3)
+
+
+def test_prefill_qwen3_shape_two_chunks():
+    """Qwen3-shaped prefill (N = 128, K = 8, d 2048, I 768): the large-batch router selection
+    (k1_select, one warp per token, kMaxN = 128 experts), 128 segment tensor maps in one GEMM
+    launch, single-CTA tiles (one 128-row tile per expert), partial cache (C < N)."""
+    S = synth.SHAPES["qwen3"]
+    m = Model(1, S.N, S.K, S.d, S.I, seed=9, gen_device="cuda")
+    ctx = _ctx(m, 512, 128.0)
+    orc = OracleEngine(1, S.N, S.K, S.d, S.I)
+    cfg = dict(v_e=48.0, seed=4)
+    ctx.configure(**cfg)
+    orc.configure(CacheConfig(**cfg))
+    _run(m, ctx, orc, synth.hidden_states(21, 2 * 384, 1, S.d), 384, 2)
