@@ -400,7 +400,11 @@ def run_ours(args, log):
                           "achieved_pcie_gbs": round(pcie_moved / (ms * 1e-3) / 1e9, 2)},
         "kernels_ms": {"router": round(k1["total_ms"], 3), "expert": round(k2["total_ms"], 3),
                        "gemm": round(kg["total_ms"], 3),
-                       "combine": round(k3["total_ms"], 3)},
+                       "combine": round(k3["total_ms"], 3),
+                       "in_kernel": {"router": round(k1["kernel_ms"], 3), "expert": round(k2["kernel_ms"], 3),
+                                     "combine": round(k3["kernel_ms"], 3),
+                                     "note": "first-CTA start to last-CTA end (%globaltimer); the event "
+                                             "times above also hold launch latency"}},
         "cache": {"alpha": dc["act_alpha"], "beta": dc["act_beta"], "gamma": dc["act_gamma"],
                   "pred_hit_rate": round(dc["pred_hits"] / max(1, dc["pred_total"]), 4)},
         "clocks": ck, "e2e": e2e,

@@ -205,11 +205,14 @@ moepic_status moepic_get_counters(moepic_ctx* ctx, moepic_counters* out);
 
 /* Kernel timing with CUDA events recorded on the launching stream around every launch of the
  * given kernel class while profiling is enabled.  bytes = algorithmic HBM bytes of those
- * launches (K2: weight rows x 6d + activations).                          */
+ * launches (K2: weight rows x 6d + activations).  kernel_ms sums, per
+ * launch, the span from the first CTA's start to the last CTA's end read from %globaltimer
+ * inside the kernels (0 for the prefill GEMMs), so total_ms - kernel_ms is launch latency.    */
 typedef struct {
   uint64_t launches;
   double total_ms;
   uint64_t bytes;
+  double kernel_ms;
 } moepic_kernel_stats;
 enum { MOEPIC_KERNEL_ROUTER = 0, MOEPIC_KERNEL_EXPERT = 1, MOEPIC_KERNEL_COMBINE = 2,
        MOEPIC_KERNEL_GEMM = 3 /* prefill tcgen05 GEMMs; `bytes` holds algorithmic FLOPs */ };

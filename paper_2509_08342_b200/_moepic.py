@@ -67,7 +67,8 @@ class moepic_counters(C.Structure):
 
 
 class moepic_kernel_stats(C.Structure):
-    _fields_ = [("launches", C.c_uint64), ("total_ms", C.c_double), ("bytes", C.c_uint64)]
+    _fields_ = [("launches", C.c_uint64), ("total_ms", C.c_double), ("bytes", C.c_uint64),
+                ("kernel_ms", C.c_double)]
 
 
 KERNEL_ROUTER, KERNEL_EXPERT, KERNEL_COMBINE, KERNEL_GEMM = 0, 1, 2, 3

@@ -193,7 +193,8 @@ class MoEpic:
     def profile_read(self, kernel_class):
         k = M.moepic_kernel_stats()
         self._err(M.moepic_profile_read(self.h, kernel_class, C.byref(k)), "moepic_profile_read")
-        return dict(launches=int(k.launches), total_ms=float(k.total_ms), bytes=int(k.bytes))
+        return dict(launches=int(k.launches), total_ms=float(k.total_ms), bytes=int(k.bytes),
+                    kernel_ms=float(k.kernel_ms))
 
     def get_stats(self) -> bytes:
         n = C.c_size_t()

@@ -15,13 +15,16 @@ struct CombineParamsCap {
   const uint16_t* h;
   const float* ws;
   int B, d, residual, nsegs;
+  unsigned long long* tstamp;
   CombineSeg segs[CAP];
 };
 
 template <class P>
 __global__ void __launch_bounds__(kCombineWarps * 32) k3_combine(const __grid_constant__ P p) {
   __shared__ float4 red[kCombineWarps * 32];
+  stamp_start(p.tstamp);
   combine_block(blockIdx.x, p.segs, p.nsegs, p.ws, p.h, p.y, p.d, p.residual, red);
+  stamp_end(p.tstamp);
 }
 
 // parameter block sized to the step (see expert.cu: launch commands cross the busy PCIe link)
@@ -29,7 +32,7 @@ template <int CAP>
 static void launch_cap(const CombineParams& p, cudaStream_t s) {
   CombineParamsCap<CAP> q;
   q.y = p.y; q.h = p.h; q.ws = p.ws;
-  q.B = p.B; q.d = p.d; q.residual = p.residual; q.nsegs = p.nsegs;
+  q.B = p.B; q.d = p.d; q.residual = p.residual; q.nsegs = p.nsegs; q.tstamp = p.tstamp;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   const int nblk = p.B * ((p.d / 4 + 31) / 32);
   k3_combine<CombineParamsCap<CAP>><<<nblk, kCombineWarps * 32, 0, s>>>(q);

@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "kernels.hpp"
+
 namespace moepic {
 // ============================================================== small helpers
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
@@ -31,6 +33,20 @@ __device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, f
       "mov.b64 {%0, %1}, rc;\n\t}"
       : "+f"(d0), "+f"(d1)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// In-kernel timestamps for moepic_profile (diagnostics): record r of the host's ring holds the
+// earliest CTA start at ts[0] and the latest CTA end at ts[kProfRing] (ns, %globaltimer).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp_start(unsigned long long* ts) {
+  if (ts && threadIdx.x == 0) atomicMin(ts, gtimer());
+}
+__device__ __forceinline__ void stamp_end(unsigned long long* ts) {
+  if (ts && threadIdx.x == 0) atomicMax(ts + kProfRing, gtimer());
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   const int64_t R = p.total_rows;
   const int64_t G = gridDim.x;
   const int64_t r0 = k2_row_lo(blockIdx.x, R, G), r1 = k2_row_lo(blockIdx.x + 1, R, G);
+  stamp_start(p.tstamp);
   if (r0 >= r1) return;
 
   if (tid == 0) {
@@ -349,6 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     for (int blk = blockIdx.x; blk < nblk; blk += G)
       combine_block(blk, p.comb, p.ncomb, p.ws, p.h, p.y, d, p.residual, red);
   }
+  __syncthreads();
+  stamp_end(p.tstamp);
 }
 
 // The kernel parameter block is sized to the launch: kernel arguments travel in the launch
@@ -366,6 +369,7 @@ struct K2ParamsCap {
   float* y;
   unsigned long long* bar;
   unsigned long long bar_target;
+  unsigned long long* tstamp;
   CombineSeg comb[CAP];
 };
 
@@ -376,7 +380,7 @@ static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0;
-  q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target;
+  q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target; q.tstamp = p.tstamp;
   for (int i = 0; i < q.ncomb; ++i) q.comb[i] = p.comb[i];
   auto* fn = k2_split_expert<TB, CW, RS, K2ParamsCap<CAP>>;
   if (p.combine) {   // grid barrier: every CTA must be co-resident

@@ -42,8 +42,10 @@ struct RouterParams {
   unsigned int* ticket2;            // zero-initialised, reset by k1_select
   int32_t* sel_cnt;                 // [N] zero-initialised, reset by k1_select
   unsigned long long* sel_max;      // [N] order-preserving max-logit keys, reset to 0
+  unsigned long long* tstamp;       // profiling record (device_utils.cuh) or nullptr
 };
 constexpr int kRouterSplitB = 32;
+constexpr int kProfRing = 4096;   // profiling records (events + in-kernel timestamps) per drain
 void launch_router(const RouterParams& p, cudaStream_t s);
 
 // ------------------------------------------------------------------ K2: split-expert stream
@@ -78,6 +80,7 @@ struct K2Params {
   float* y;
   unsigned long long* bar;
   unsigned long long bar_target;
+  unsigned long long* tstamp;       // profiling record or nullptr
   CombineSeg comb[kMaxLaunchSegs];
 };
 // Partition rule shared with the host: CTA c of G owns launch rows [c*R/G, (c+1)*R/G).
@@ -93,6 +96,7 @@ struct CombineParams {
   const uint16_t* h;      // residual source
   const float* ws;
   int B, d, residual, nsegs;
+  unsigned long long* tstamp;       // profiling record or nullptr
   CombineSeg segs[kMaxStepSegs];
 };
 void launch_combine(const CombineParams& p, cudaStream_t s);

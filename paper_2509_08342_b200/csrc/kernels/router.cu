@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
   const int BN = p.B * p.N;
   const int total = BN * 2;
   const int n_chunks = p.d >> 3;
+  stamp_start(p.tstamp);
 
   // ---- phase 1: one warp per (matrix, token, expert) logit
   const int gw = blockIdx.x * nwarps + warp;
@@ -86,7 +87,10 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
       if (lane == 0) p.logits[(size_t)m * BN + rem] = acc;
     }
   }
-  if (p.B > kRouterSplitB) return;   // large batch: k1_select does phases 2 and 3
+  if (p.B > kRouterSplitB) {   // large batch: k1_select does phases 2 and 3
+    stamp_end(p.tstamp);
+    return;
+  }
   // ---- the last CTA to finish phase 1 does the selection
   __threadfence();
   __syncthreads();
@@ -95,7 +99,10 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) {
+    stamp_end(p.tstamp);
+    return;
+  }
   __threadfence();
   const double* L0 = p.logits;
   const double* L1 = p.logits + BN;
@@ -168,6 +175,7 @@ __global__ void __launch_bounds__(256) k1_router(RouterParams p) {
     for (int i = threadIdx.x; i < p.N; i += blockDim.x) p.mb_rank[i] = tag | (uint32_t)p.ranking[i];
   }
   if (threadIdx.x == 0) *p.ticket = 0u;
+  stamp_end(p.tstamp);
 }
 
 // order-preserving map double -> u64 (larger double <-> larger key; 0 is below every logit)
@@ -194,6 +202,7 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
   const double* L1 = p.logits + BN;
   const unsigned long long tag = (unsigned long long)p.seq << 32;
   const int b = blockIdx.x * 8 + warp;
+  stamp_start(p.tstamp);
   for (int j = threadIdx.x; j < p.N; j += blockDim.x) {
     s_cnt[j] = 0;
     s_max[j] = 0ull;
@@ -235,7 +244,10 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
       }
     }
   }
-  if (p.W1 == nullptr) return;
+  if (p.W1 == nullptr) {
+    stamp_end(p.tstamp);
+    return;
+  }
   __syncthreads();
   for (int j = threadIdx.x; j < p.N; j += blockDim.x) {   // one global atomic per expert per CTA
     if (s_cnt[j]) atomicAdd(&p.sel_cnt[j], s_cnt[j]);
@@ -248,7 +260,10 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) {
+    stamp_end(p.tstamp);
+    return;
+  }
   __threadfence();
   // ranking: key = (count desc, max logit desc, id asc)
   const int nwarps = blockDim.x >> 5;
@@ -275,6 +290,7 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
     p.sel_max[i] = 0ull;
   }
   if (threadIdx.x == 0) *p.ticket2 = 0u;
+  stamp_end(p.tstamp);
 }
 
 void launch_router(const RouterParams& p, cudaStream_t s) {

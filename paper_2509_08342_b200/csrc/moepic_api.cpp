@@ -37,7 +37,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
-  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, total;
+  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, total;
   uint64_t pool_rows, plan_rows, od_rows, ws_floats;
   // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
   size_t xperm, aact, yperm, pos, cursor;
@@ -89,6 +89,7 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   a.ranking = off; off = align_up(off + (size_t)d.N * 4);
   a.ticket = off; off = align_up(off + 64);
   a.rsel = off; off = align_up(off + (size_t)d.N * 16);   // k1_select: cnt int32 [N] | max u64 [N]
+  a.trec = off; off = align_up(off + (size_t)2 * kProfRing * 8);   // profiling: start [ring] | end [ring]
   a.pf_rows = 0;
   a.xperm = a.aact = a.yperm = a.pos = a.cursor = off;
   if (d.max_batch > kDecodeMaxB) {
@@ -290,9 +291,24 @@ struct moepic_ctx {
     if (idx < 0) return;
     prof[idx].bytes = bytes;
     cudaEventRecord(prof[idx].b, s);
-    if (prof_used >= 4096) prof_drain();
+    if (prof_used >= (size_t)kProfRing) prof_drain();
+  }
+  // in-kernel timestamp record of profiling slot idx (device_utils.cuh), nullptr when off
+  unsigned long long* tstamp(int idx) const {
+    return idx < 0 ? nullptr : reinterpret_cast<unsigned long long*>(arena + lay.trec) + idx;
+  }
+  void tstamp_reset(size_t n) {
+    if (n == 0) return;
+    cudaMemset(arena + lay.trec, 0xFF, n * 8);
+    cudaMemset(arena + lay.trec + (size_t)kProfRing * 8, 0, n * 8);
   }
   void prof_drain() {
+    std::vector<unsigned long long> ts(prof_used), te(prof_used);
+    if (prof_used) {
+      cudaDeviceSynchronize();
+      cudaMemcpy(ts.data(), arena + lay.trec, prof_used * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(te.data(), arena + lay.trec + (size_t)kProfRing * 8, prof_used * 8, cudaMemcpyDeviceToHost);
+    }
     for (size_t i = 0; i < prof_used; ++i) {
       float ms = 0.f;
       cudaEventSynchronize(prof[i].b);
@@ -301,7 +317,10 @@ struct moepic_ctx {
       k.launches++;
       k.total_ms += ms;
       k.bytes += prof[i].bytes;
+      if (te[i] > ts[i] && ts[i] != ~0ull) k.kernel_ms += (double)(te[i] - ts[i]) * 1e-6;
     }
+    tstamp_reset(prof_used);
+    if (prof_used) cudaDeviceSynchronize();
     prof_used = 0;
   }
   std::vector<int32_t> ids_h, rank_h;
@@ -595,6 +614,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       fuse->done = true;
     }
     const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
+    kp.tstamp = ctx->tstamp(pe);
     launch_k2(kp, (int)G, tb, s);
     ctx->prof_end(pe, s, alg_bytes);
     CK(cudaGetLastError());
@@ -673,6 +693,7 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   rp.seq = ++ctx->seq;
   rp.B = B; rp.d = d.d; rp.N = d.N; rp.K = d.K; rp.renorm = d.renorm_topk;
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_ROUTER);
+  rp.tstamp = ctx->tstamp(pe);
   launch_router(rp, s);
   ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
   CK(cudaGetLastError());
@@ -1070,6 +1091,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   cpar.nsegs = (int)comb.size();
   for (size_t i = 0; i < comb.size(); ++i) cpar.segs[i] = comb[i];
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_COMBINE);
+  cpar.tstamp = ctx->tstamp(pe);
   launch_combine(cpar, s);
   {
     uint64_t cb = (uint64_t)B * d.d * 4;
@@ -1259,6 +1281,10 @@ moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable) {
   ctx->prof_drain();
   for (auto& k : ctx->prof_acc) k = moepic_kernel_stats{};
   ctx->profiling = enable != 0;
+  if (ctx->profiling) {
+    ctx->tstamp_reset(kProfRing);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(&ctx->err, MOEPIC_ERUNTIME, "profile reset failed");
+  }
   return MOEPIC_OK;
 }
 

@@ -69,7 +69,9 @@ def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
                k2_launches_per_layer=k2["launches"] / n,
                k2_MB=round(k2["bytes"] / max(1, k2["launches"]) / 1e6, 2),
                k2_GBps=round(k2["bytes"] / (k2["total_ms"] * 1e-3) / 1e9, 1),
+               k2_kernel_us=round(k2["kernel_ms"] * 1e3 / max(1, k2["launches"]), 2),
                k1_us=round(k1["total_ms"] * 1e3 / max(1, k1["launches"]), 2),
+               k1_kernel_us=round(k1["kernel_ms"] * 1e3 / max(1, k1["launches"]), 2),
                k3_us=round(k3["total_ms"] * 1e3 / max(1, k3["launches"]), 2),
                layer_GBps=round(k2["bytes"] / n / (ms * 1e-3 / n) / 1e9, 1))
     ctx.close()
