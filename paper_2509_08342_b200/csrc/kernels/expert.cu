@@ -295,12 +295,18 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       if (prev_seg != s) flush(prev_seg, prev_ntok);
     }
 
-    // ---- finalise a = silu(g) * u * w for this tile (every warp, fixed order)
+    // ---- finalise a = silu(g) * u * w for this tile (every warp, fixed tree)
+    // lane l sums value l % NV over the warps w = l / NV (mod 32 / NV) in order, then a butterfly
+    // over the lane groups: a short chain instead of 16 dependent adds on every tile
     mbar_wait(&redbar[n & 1], (n >> 1) & 1);
     float sum = 0.f;
-    if (lane < NV) {
-#pragma unroll 4
-      for (int w2 = 0; w2 < kConsumerWarps; ++w2) sum += rb[w2 * NV + lane];
+    {
+      constexpr int NG = 32 / NV;                  // lane groups
+      const int v = lane % NV, g0 = lane / NV;
+#pragma unroll
+      for (int w2 = g0; w2 < kConsumerWarps; w2 += NG) sum += rb[w2 * NV + v];
+#pragma unroll
+      for (int o = NV; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     }
     const float upart = __shfl_sync(0xffffffffu, sum, (lane + RS * TB) & 31);
     float a = 0.f;
