@@ -38,6 +38,17 @@ static void launch_cap(const CombineParams& p, cudaStream_t s) {
   k3_combine<CombineParamsCap<CAP>><<<nblk, kCombineWarps * 32, 0, s>>>(q);
 }
 
+cudaError_t combine_init() {
+  cudaError_t e = cudaSuccess, r;
+  if ((r = cudaFuncSetAttribute(k3_combine<CombineParamsCap<16>>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                100)) != cudaSuccess) e = r;
+  if ((r = cudaFuncSetAttribute(k3_combine<CombineParamsCap<128>>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                100)) != cudaSuccess) e = r;
+  if ((r = cudaFuncSetAttribute(k3_combine<CombineParamsCap<kMaxStepSegs>>,
+                                cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) e = r;
+  return e;
+}
+
 void launch_combine(const CombineParams& p, cudaStream_t s) {
   if (p.nsegs <= 16) launch_cap<16>(p, s);
   else if (p.nsegs <= 128) launch_cap<128>(p, s);

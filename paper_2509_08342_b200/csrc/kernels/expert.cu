@@ -15,9 +15,10 @@
 //                 warp butterfly, lane 0 stores the warp partials, warp arrives on `red[t&1]`;
 //       phase 2   of the PREVIOUS tile: y_partial[tok][cols] += a[r][tok] * down_r[cols], then the
 //                 warp releases that stage (this work hides the reduction barrier);
-//       finalise  wait `red[t&1]`; every warp sums the 16 warp partials in warp order (fixed,
-//                 deterministic), a = silu(g) * u * w_gate (fp32), broadcast by shuffles.
-//   Per (segment, CTA) partials are written once to the workspace; K3 adds them in a fixed order.
+//       finalise  wait `red[t&1]`; every warp sums the 16 warp partials with a fixed lane tree
+//                 (deterministic), a = silu(g) * u * w_gate (fp32), broadcast by shuffles.
+//   Per (segment, CTA) partials are written once to the workspace; the step's final launch
+//   combines them after a grid barrier (combine_dev.cuh, fixed order), else K3 does.
 // Decode has <= 4 tokens per expert (B K / N): CUDA-core FMA at <= 8 flop/byte, HBM-bound; tensor
 // cores are for prefill.
 #include "kernels.hpp"
@@ -448,6 +449,8 @@ bool kernels_init(char* err, size_t errlen) {
   MOEPIC_ATTR(1, 4, 8) MOEPIC_ATTR(2, 4, 8)
   MOEPIC_ATTR(1, 4, 16)
 #undef MOEPIC_ATTR
+  if ((r = router_init()) != cudaSuccess) e = r;
+  if ((r = combine_init()) != cudaSuccess) e = r;
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return false;

@@ -47,6 +47,8 @@ struct RouterParams {
 constexpr int kRouterSplitB = 32;
 constexpr int kProfRing = 4096;   // profiling records (events + in-kernel timestamps) per drain
 void launch_router(const RouterParams& p, cudaStream_t s);
+cudaError_t router_init();     // shared-memory carveout hints (called by kernels_init)
+cudaError_t combine_init();
 
 // ------------------------------------------------------------------ K2: split-expert stream
 struct Seg {

@@ -293,6 +293,14 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
   stamp_end(p.tstamp);
 }
 
+// Small kernels run between K2 launches that need ~200 KB of shared memory: asking for the
+// maximum shared-memory carveout keeps the SM's L1/shared split unchanged between them.
+cudaError_t router_init() {
+  cudaError_t e = cudaFuncSetAttribute(k1_router, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaError_t f = cudaFuncSetAttribute(k1_select, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  return e != cudaSuccess ? e : f;
+}
+
 void launch_router(const RouterParams& p, cudaStream_t s) {
   const int warps = 2 * p.B * p.N;
   const int grid = (warps + 7) / 8;
