@@ -2,6 +2,8 @@
 // their per-CTA partials, in a fixed order (deterministic).  Used when no K2 launch of the step
 // could fuse the combine.
 #include "kernels.hpp"
+
+#include <algorithm>
 #include "device_utils.cuh"
 #include "combine_dev.cuh"
 
@@ -36,6 +38,18 @@ static void launch_cap(const CombineParams& p, cudaStream_t s) {
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   const int nblk = p.B * ((p.d / 4 + 31) / 32);
   k3_combine<CombineParamsCap<CAP>><<<nblk, kCombineWarps * 32, 0, s>>>(q);
+}
+
+__global__ void __launch_bounds__(256) k0_stage_in(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                   size_t n16) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s) {
+  const size_t n16 = bytes / 16;
+  const int grid = (int)std::min<size_t>((n16 + 255) / 256, 64);
+  k0_stage_in<<<grid, 256, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src_mapped), n16);
 }
 
 cudaError_t combine_init() {

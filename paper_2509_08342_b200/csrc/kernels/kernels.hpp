@@ -103,6 +103,11 @@ struct CombineParams {
 };
 void launch_combine(const CombineParams& p, cudaStream_t s);
 
+// Host-buffer entry (moepic_layer_forward_host): copy the step's input rows from mapped pinned
+// host memory into device memory with SM loads, so the few KB do not queue behind the transfer
+// engine's multi-MB chunks on the host->device copy engine.  bytes % 16 == 0.
+void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
+
 bool kernels_init(char* err, size_t errlen);  // sets smem attributes; returns false on failure
 
 }  // namespace moepic

@@ -1164,9 +1164,11 @@ moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const ui
     if (ctx->scratch_h) cudaFreeHost(ctx->scratch_h);
     ctx->scratch_h = nullptr;
     ctx->scratch_bytes = 0;
-    CK(cudaHostAlloc(&ctx->scratch_h, need, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->scratch_h, need, cudaHostAllocMapped));
     ctx->scratch_bytes = need;
   }
+  uint8_t* scratch_d = nullptr;   // device alias of the mapped pinned staging
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&scratch_d), ctx->scratch_h, 0));
   if (ctx->dev_stage_bytes < need) {
     if (ctx->dev_stage) cudaFree(ctx->dev_stage);
     ctx->dev_stage = nullptr;
@@ -1174,13 +1176,15 @@ moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const ui
     CK(cudaMalloc(&ctx->dev_stage, need));
     ctx->dev_stage_bytes = need;
   }
+  // h: host -> mapped pinned staging -> device (SM loads, not the busy H2D copy engine);
+  // y: the combine stores straight into the mapped staging (zero-copy), read after the sync
   memcpy(ctx->scratch_h + hoff, h_host, hb);
   uint8_t* ds = static_cast<uint8_t*>(ctx->dev_stage);
-  CK(cudaMemcpyAsync(ds + hoff, ctx->scratch_h + hoff, hb, cudaMemcpyHostToDevice, s));
-  moepic_status st = moepic_layer_forward(ctx, layer, ds + hoff, B, reinterpret_cast<float*>(ds + yoff), stream,
-                                          flags, tr);
+  launch_stage_in(ds + hoff, scratch_d + hoff, align_up(hb), s);
+  CK(cudaGetLastError());
+  moepic_status st = moepic_layer_forward(ctx, layer, ds + hoff, B, reinterpret_cast<float*>(scratch_d + yoff),
+                                          stream, flags, tr);
   if (st != MOEPIC_OK) return st;
-  CK(cudaMemcpyAsync(ctx->scratch_h + yoff, ds + yoff, yb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   memcpy(y_host, ctx->scratch_h + yoff, yb);
   return MOEPIC_OK;

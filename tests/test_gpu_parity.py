@@ -240,6 +240,30 @@ def test_host_buffers_and_predict_prefetch():
             assert rel_err(y, y_ref) <= TOL
 
 
+@pytest.mark.parametrize("B", [3, 40])
+def test_host_buffers_batches(B):
+    """Host-buffer entry for a decode batch and a prefill batch (h staged by SM loads from mapped
+    pinned memory, y stored zero-copy into mapped pinned memory)."""
+    api = _api()
+    m = Model(2, 8, 2, 256, 512, n_shared=1, seed=18)
+    ctx = _ctx(m, max_batch=B, v_e_max=8.0)
+    orc = OracleEngine(2, 8, 2, 256, 512, n_shared=1)
+    cfg = dict(v_e=4.0, seed=2)
+    ctx.configure(**cfg)
+    orc.configure(CacheConfig(**cfg))
+    H = synth.hidden_states(19, 2 * B, 2, 256)
+    for t in range(2):
+        for i in range(2):
+            hb = synth.bf16_bits(H[t * B:(t + 1) * B, i])
+            y, tr = ctx.layer_forward_host(i, hb, flags=api.M.FUSE_PREDICT)
+            y_ref, ids, _, _ = m.oracle_layer(i, hb)
+            assert np.array_equal(tr.ids, ids)
+            nrank = ON.predicted_ranking(ON.router_logits(hb, m.routers[(i + 1) % 2]), 2)
+            o = orc.step(i, ids, (i + 1) % 2, nrank)
+            assert tr.act == o.act and tr.adm == o.adm and tr.plan == o.plan
+            assert rel_err(y, y_ref) <= TOL
+
+
 def test_residual_flag_and_errors():
     api = _api()
     m = Model(2, 8, 2, 64, 128, seed=2)
