@@ -37,7 +37,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
-  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, total;
+  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, hstage, total;
   uint64_t pool_rows, plan_rows, od_rows, ws_floats;
   // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
   size_t xperm, aact, yperm, pos, cursor;
@@ -90,6 +90,7 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   a.ticket = off; off = align_up(off + 64);
   a.rsel = off; off = align_up(off + (size_t)d.N * 16);   // k1_select: cnt int32 [N] | max u64 [N]
   a.trec = off; off = align_up(off + (size_t)2 * kProfRing * 8);   // profiling: start [ring] | end [ring]
+  a.hstage = off; off = align_up(off + (size_t)d.max_batch * d.d * 2);   // layer_forward_host input rows
   a.pf_rows = 0;
   a.xperm = a.aact = a.yperm = a.pos = a.cursor = off;
   if (d.max_batch > kDecodeMaxB) {
@@ -325,10 +326,9 @@ struct moepic_ctx {
   }
   std::vector<int32_t> ids_h, rank_h;
   std::vector<float> w_h;
-  uint8_t* scratch_h = nullptr;      // pinned staging for *_host calls
+  uint8_t* scratch_h = nullptr;      // mapped pinned staging for *_host calls (h | y), sized at create
+  uint8_t* scratch_d = nullptr;      // its device alias
   size_t scratch_bytes = 0;
-  void* dev_stage = nullptr;         // device staging for *_host calls
-  size_t dev_stage_bytes = 0;
 
   uint64_t rb() const { return 6ull * desc.d; }
   int Nl() const { return n_local(desc); }
@@ -397,6 +397,10 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
     return st;
   };
   if (!kernels_init(kerr, sizeof kerr)) return bail(MOEPIC_ERUNTIME);
+  ctx->scratch_bytes = align_up((size_t)desc->max_batch * desc->d * 2) + (size_t)desc->max_batch * desc->d * 4;
+  if (cudaHostAlloc(&ctx->scratch_h, ctx->scratch_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->scratch_d), ctx->scratch_h, 0) != cudaSuccess)
+    return bail(MOEPIC_ENOMEM);
   if (desc->max_batch > kDecodeMaxB && !prefill_init(kerr, sizeof kerr)) return bail(MOEPIC_ERUNTIME);
   const uint64_t host_bytes = (uint64_t)desc->L_host * ctx->Nl() * desc->I * ctx->rb();
   if (cudaHostAlloc(&ctx->host_experts, host_bytes, cudaHostAllocDefault) != cudaSuccess) {
@@ -1158,31 +1162,15 @@ moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const ui
   if (B < 1 || B > d.max_batch) return fail(&ctx->err, MOEPIC_EINVAL, "B must be in [1, max_batch]");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t hb = (size_t)B * d.d * 2, yb = (size_t)B * d.d * 4;
-  const size_t hoff = 0, yoff = align_up(hb);
-  const size_t need = yoff + yb;
-  if (ctx->scratch_bytes < need) {
-    if (ctx->scratch_h) cudaFreeHost(ctx->scratch_h);
-    ctx->scratch_h = nullptr;
-    ctx->scratch_bytes = 0;
-    CK(cudaHostAlloc(&ctx->scratch_h, need, cudaHostAllocMapped));
-    ctx->scratch_bytes = need;
-  }
-  uint8_t* scratch_d = nullptr;   // device alias of the mapped pinned staging
-  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&scratch_d), ctx->scratch_h, 0));
-  if (ctx->dev_stage_bytes < need) {
-    if (ctx->dev_stage) cudaFree(ctx->dev_stage);
-    ctx->dev_stage = nullptr;
-    ctx->dev_stage_bytes = 0;
-    CK(cudaMalloc(&ctx->dev_stage, need));
-    ctx->dev_stage_bytes = need;
-  }
-  // h: host -> mapped pinned staging -> device (SM loads, not the busy H2D copy engine);
-  // y: the combine stores straight into the mapped staging (zero-copy), read after the sync
-  memcpy(ctx->scratch_h + hoff, h_host, hb);
-  uint8_t* ds = static_cast<uint8_t*>(ctx->dev_stage);
-  launch_stage_in(ds + hoff, scratch_d + hoff, align_up(hb), s);
+  const size_t yoff = align_up((size_t)d.max_batch * d.d * 2);
+  // h: host -> mapped pinned staging -> arena (SM loads, not the busy H2D copy engine);
+  // y: the combine stores straight into the mapped staging (zero-copy), read after the sync.
+  // Both buffers are allocated at create, so no allocation happens on this path.
+  memcpy(ctx->scratch_h, h_host, hb);
+  uint8_t* ds = ctx->arena + ctx->lay.hstage;
+  launch_stage_in(ds, ctx->scratch_d, (hb + 15) / 16 * 16, s);
   CK(cudaGetLastError());
-  moepic_status st = moepic_layer_forward(ctx, layer, ds + hoff, B, reinterpret_cast<float*>(scratch_d + yoff),
+  moepic_status st = moepic_layer_forward(ctx, layer, ds, B, reinterpret_cast<float*>(ctx->scratch_d + yoff),
                                           stream, flags, tr);
   if (st != MOEPIC_OK) return st;
   CK(cudaStreamSynchronize(s));
@@ -1318,7 +1306,6 @@ void moepic_destroy(moepic_ctx* ctx) {
   if (ctx->host_experts) cudaFreeHost(ctx->host_experts);
   if (ctx->mailbox) cudaFreeHost(ctx->mailbox);
   if (ctx->scratch_h) cudaFreeHost(ctx->scratch_h);
-  if (ctx->dev_stage) cudaFree(ctx->dev_stage);
   delete ctx;
 }
 
