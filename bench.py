@@ -530,7 +530,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="tokens timed on the host-buffer path (default: --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=None, help="override the config's decode batch")
     ap.add_argument("--tau", type=int, default=64, help="tokens per Alg. 1 period (adaptive configs)")
@@ -542,6 +542,8 @@ def main():
                     help="gloo lets several ranks share one GPU (multi-rank test on a 1-GPU box)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
     if args.batch:
         CONFIGS[args.config]["B"] = args.batch
     if args.no_adapt:

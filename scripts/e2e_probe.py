@@ -17,6 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="deepseek")
     ap.add_argument("--tokens", type=int, default=4)
+    ap.add_argument("--adapt", type=int, default=0, help="tokens of the Alg. 1 profiling phase (bench: 128)")
     a = ap.parse_args()
     import torch
     import synth
@@ -26,7 +27,7 @@ def main():
     ctx, desc, S, v_e, keep = bench.build_model(api, synth, torch, cfg, max_batch=cfg["B"], log=lambda *x: None)
     L, B = cfg["L"], cfg["B"]
     ctx.configure(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
-    T = 4 * a.tokens + 4
+    T = 4 * a.tokens + 4 + a.adapt
     H = synth.hidden_states(1, T * B, L, S.d).permute(1, 0, 2).contiguous().to("cuda")
     Hh = H.cpu()
     y = torch.empty(B, S.d, dtype=torch.float32, device="cuda")
@@ -50,6 +51,17 @@ def main():
         torch.cuda.synchronize()
         return (time.perf_counter() - t0) / (ntok * L) * 1e6
 
+    if a.adapt:   # the bench's Alg. 1 step (bench.py run_ours)
+        ctx.profile(True)
+        run("device", a.adapt)
+        k2w = ctx.profile_read(api.M.KERNEL_EXPERT)
+        ctx.profile(False)
+        pcie = bench.pcie_probe(torch)
+        t_load = 6 * S.d * S.I / (pcie * 1e9) * 1e3
+        t_moe = k2w["total_ms"] / (a.adapt * L)
+        r = ctx.configure(use_solver=True, t_att=0.0, t_moe=t_moe, t_head=0.0, t_load_exp=t_load, zeta=0.01,
+                          v_e=v_e, y_cap_i=[S.K * B] * L, seed=0)
+        print("theta", min(r["theta_eff_i"]), max(r["theta_eff_i"]), flush=True)
     run("device", 2)
     for mode in ("device", "sync", "host", "device"):
         print(f"{a.config} {mode:7s} {run(mode, a.tokens):8.1f} us/layer", flush=True)
