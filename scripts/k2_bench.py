@@ -44,6 +44,7 @@ def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
         for i in range(L):
             ctx.layer_forward(i, hsel(t, i), y, stream=st, trace=False)
     torch.cuda.synchronize()
+    ctx.profile(True)   # (resets with a device sync: start the background load after it)
     if pcie_load:   # saturate the H2D link with a background copy loop on another stream
         hsrc = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
         hdst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
@@ -51,7 +52,6 @@ def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
         with torch.cuda.stream(bg):
             for _ in range(4 + steps // 4):
                 hdst.copy_(hsrc, non_blocking=True)
-    ctx.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for t in range(5, steps + 5):
