@@ -20,7 +20,7 @@ import synth  # noqa: E402
 from paper_2509_08342_b200 import api  # noqa: E402
 
 
-def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
+def run(shape, B, steps, L=2, theta=1.0, pcie_load=False, profile=True):
     S = synth.SHAPES[shape]
     desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=64, max_batch=B,
                           renorm_topk=S.renorm, L_host=1, v_e_max=L * S.N)
@@ -44,7 +44,7 @@ def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
         for i in range(L):
             ctx.layer_forward(i, hsel(t, i), y, stream=st, trace=False)
     torch.cuda.synchronize()
-    ctx.profile(True)   # (resets with a device sync: start the background load after it)
+    ctx.profile(profile)   # (resets with a device sync: start the background load after it)
     if pcie_load:   # saturate the H2D link with a background copy loop on another stream
         hsrc = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
         hdst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
@@ -68,7 +68,7 @@ def run(shape, B, steps, L=2, theta=1.0, pcie_load=False):
                k2_us=round(k2["total_ms"] * 1e3 / max(1, k2["launches"]), 2),
                k2_launches_per_layer=k2["launches"] / n,
                k2_MB=round(k2["bytes"] / max(1, k2["launches"]) / 1e6, 2),
-               k2_GBps=round(k2["bytes"] / (k2["total_ms"] * 1e-3) / 1e9, 1),
+               k2_GBps=round(k2["bytes"] / max(k2["total_ms"] * 1e-3, 1e-12) / 1e9, 1),
                k2_kernel_us=round(k2["kernel_ms"] * 1e3 / max(1, k2["launches"]), 2),
                k1_us=round(k1["total_ms"] * 1e3 / max(1, k1["launches"]), 2),
                k1_kernel_us=round(k1["kernel_ms"] * 1e3 / max(1, k1["launches"]), 2),
@@ -83,10 +83,12 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--cases", default="mixtral:1,qwen3:1,qwen3:4,qwen3:16,deepseek:1")
     ap.add_argument("--pcie-load", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="no per-kernel events (layer_us only)")
     args = ap.parse_args()
     for c in args.cases.split(","):
         shape, B = c.split(":")
-        print(json.dumps(run(shape, int(B), args.steps, pcie_load=args.pcie_load)), flush=True)
+        print(json.dumps(run(shape, int(B), args.steps, pcie_load=args.pcie_load, profile=not args.no_profile)),
+              flush=True)
 
 
 if __name__ == "__main__":
