@@ -9,7 +9,7 @@
 
 namespace moepic {
 
-// One CTA of 16 warps per (token, 32-float4 column block): combine_dev.cuh, the same order as
+// One CTA of 16 warps per (token, column block): combine_dev.cuh, the same order as
 // the fused combine at the end of the final K2 launch.
 template <int CAP>
 struct CombineParamsCap {
@@ -25,7 +25,7 @@ template <class P>
 __global__ void __launch_bounds__(kCombineWarps * 32) k3_combine(const __grid_constant__ P p) {
   __shared__ float4 red[kCombineWarps * 32];
   stamp_start(p.tstamp);
-  combine_block(blockIdx.x, p.segs, p.nsegs, p.ws, p.h, p.y, p.d, p.residual, red);
+  combine_block(blockIdx.x, p.segs, p.nsegs, p.ws, p.h, p.y, p.B, p.d, p.residual, red);
   stamp_end(p.tstamp);
 }
 
@@ -36,7 +36,7 @@ static void launch_cap(const CombineParams& p, cudaStream_t s) {
   q.y = p.y; q.h = p.h; q.ws = p.ws;
   q.B = p.B; q.d = p.d; q.residual = p.residual; q.nsegs = p.nsegs; q.tstamp = p.tstamp;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
-  const int nblk = p.B * ((p.d / 4 + 31) / 32);
+  const int nblk = combine_blocks(p.B, p.d);
   k3_combine<CombineParamsCap<CAP>><<<nblk, kCombineWarps * 32, 0, s>>>(q);
 }
 

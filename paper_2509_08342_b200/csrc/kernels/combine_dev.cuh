@@ -3,10 +3,12 @@
 //
 // y[b][c] = (h[b][c] if residual) + sum over the partial vectors serving token b.  The partials
 // of token b are enumerated in a fixed order (segments in step order, chunks in CTA order) and
-// numbered k = 0, 1, ...; warp w of the 16 sums the k = w (mod 16) ones in increasing k with its
-// lanes on 32 consecutive float4 columns (coalesced), and the 16 warp sums are added in warp
-// order.  The order depends only on the step's segment table, so the result is deterministic
-// and identical for the fused and the stand-alone combine.
+// numbered k = 0, 1, ...  A block covers CB consecutive float4 columns of one token; lane l of
+// warp w takes column l % CB and the partials k = w * P + l / CB (mod 16 P), P = 32 / CB, in
+// increasing k; the P lane phases are added by a butterfly, then the 16 warp sums in warp order.
+// CB (32, 16, 8 or 4) is chosen from the output size only (combine_cb), so small outputs still
+// spread over the whole grid; the order depends only on the step's segment table and the
+// output shape, so the result is deterministic.
 #pragma once
 
 #include "kernels.hpp"
@@ -16,16 +18,31 @@ namespace moepic {
 
 constexpr int kCombineWarps = 16;
 
-// Column block `blk` of B * ceil(d / 128): token b = blk / ncb, float4 columns [32 cb, 32 cb + 32).
+// float4 columns per block: the widest that still yields >= 128 blocks (all SMs busy)
+__host__ __device__ inline int combine_cb(int B, int d) {
+  const int d4 = d >> 2;
+  int cb = 32;
+  while (cb > 4 && (int64_t)B * ((d4 + cb - 1) / cb) < 128) cb >>= 1;
+  return cb;
+}
+__host__ __device__ inline int combine_blocks(int B, int d) {
+  const int cb = combine_cb(B, d);
+  return B * (((d >> 2) + cb - 1) / cb);
+}
+
 // Must be called by all kCombineWarps * 32 threads of the block; `red` is 16 * 32 float4 of smem.
 __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, int nsegs, const float* ws,
-                                              const uint16_t* h, float* y, int d, int residual,
+                                              const uint16_t* h, float* y, int B, int d, int residual,
                                               float4* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d4 = d >> 2;
-  const int ncb = (d4 + 31) >> 5;
+  const int CB = combine_cb(B, d);
+  const int P = 32 / CB;                        // lane phases over the partials
+  const int S = kCombineWarps * P;              // partial stride of one lane
+  const int ncb = (d4 + CB - 1) / CB;
   const int b = blk / ncb;
-  const int c4 = (blk - b * ncb) * 32 + lane;
+  const int c4 = (blk - b * ncb) * CB + (lane % CB);
+  const int phase = warp * P + lane / CB;       // this lane's residue class mod S
   const bool active = c4 < d4;
   const uint32_t bit = 1u << b;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -37,28 +54,35 @@ __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, i
     const int t = __popc(sg.tok_mask & (bit - 1u));
     const int64_t stride4 = (int64_t)ntok * d4;
     const float4* base = reinterpret_cast<const float4*>(ws + sg.ws_off + (int64_t)t * d) + c4;
-    int ci = (warp - k0) & (kCombineWarps - 1);   // first chunk with k = w (mod 16)
+    int ci = ((phase - k0) % S + S) % S;        // first chunk with k = phase (mod S)
     if (active) {
-      for (; ci + 3 * kCombineWarps < sg.nchunks; ci += 4 * kCombineWarps) {   // 4 loads in flight
+      for (; ci + 3 * S < sg.nchunks; ci += 4 * S) {   // 4 loads in flight
         const float4 v0 = base[(int64_t)ci * stride4];
-        const float4 v1 = base[(int64_t)(ci + kCombineWarps) * stride4];
-        const float4 v2 = base[(int64_t)(ci + 2 * kCombineWarps) * stride4];
-        const float4 v3 = base[(int64_t)(ci + 3 * kCombineWarps) * stride4];
+        const float4 v1 = base[(int64_t)(ci + S) * stride4];
+        const float4 v2 = base[(int64_t)(ci + 2 * S) * stride4];
+        const float4 v3 = base[(int64_t)(ci + 3 * S) * stride4];
         acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
         acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
         acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
         acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
       }
-      for (; ci < sg.nchunks; ci += kCombineWarps) {
+      for (; ci < sg.nchunks; ci += S) {
         const float4 v = base[(int64_t)ci * stride4];
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
     }
     k0 += sg.nchunks;
   }
+  // lane phases (lanes CB apart) by a butterfly
+  for (int o = CB; o < 32; o <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
   red[warp * 32 + lane] = acc;
   __syncthreads();
-  if (warp == 0 && active) {
+  if (warp == 0 && lane < CB && active) {
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
     if (residual) {
       const uint2 hv = reinterpret_cast<const uint2*>(h + (size_t)b * d)[c4];

@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   const int64_t G = gridDim.x;
   const int64_t r0 = k2_row_lo(blockIdx.x, R, G), r1 = k2_row_lo(blockIdx.x + 1, R, G);
   stamp_start(p.tstamp);
+  unsigned long long* dbg = p.dbg ? p.dbg + (size_t)blockIdx.x * 8 : nullptr;   // phase trace (tools)
+  if (dbg && tid == 0) dbg[0] = gtimer();
   if (r0 >= r1) return;
 
   if (tid == 0) {
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       }
     }
     mbar_wait(&full[st], (n / kStagesV2) & 1);
+    if (dbg && n == 0 && tid == 0) dbg[1] = gtimer();
     const uint8_t* tile = stages + (size_t)st * tileb;
 
     // ---- phase 1: partial gate / up dots
@@ -335,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     phase2();
     flush(prev_seg, prev_ntok);
   }
+  if (dbg && tid == 0) dbg[2] = gtimer();
 
   // ---------------------------------------------------------------- fused combine (final launch)
   if (p.combine) {
@@ -350,14 +354,16 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       __threadfence();
     }
     __syncthreads();
+    if (dbg && tid == 0) dbg[3] = gtimer();
     // CTA c combines column blocks c, c + G, ... (combine_dev.cuh: 16 warps over the partials,
     // lanes over 32 float4 columns, fixed order); the K2 smem ring is free again here
     float4* red = reinterpret_cast<float4*>(smem);
-    const int nblk = p.B * ((((d >> 2)) + 31) >> 5);
+    const int nblk = combine_blocks(p.B, d);
     for (int blk = blockIdx.x; blk < nblk; blk += G)
-      combine_block(blk, p.comb, p.ncomb, p.ws, p.h, p.y, d, p.residual, red);
+      combine_block(blk, p.comb, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red);
   }
   __syncthreads();
+  if (dbg && tid == 0) dbg[4] = gtimer();
   stamp_end(p.tstamp);
 }
 
@@ -377,6 +383,7 @@ struct K2ParamsCap {
   unsigned long long* bar;
   unsigned long long bar_target;
   unsigned long long* tstamp;
+  unsigned long long* dbg;
   CombineSeg comb[CAP];
 };
 
@@ -387,7 +394,7 @@ static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0;
-  q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target; q.tstamp = p.tstamp;
+  q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target; q.tstamp = p.tstamp; q.dbg = p.dbg;
   for (int i = 0; i < q.ncomb; ++i) q.comb[i] = p.comb[i];
   auto* fn = k2_split_expert<TB, CW, RS, K2ParamsCap<CAP>>;
   if (p.combine) {   // grid barrier: every CTA must be co-resident

@@ -83,6 +83,7 @@ struct K2Params {
   unsigned long long* bar;
   unsigned long long bar_target;
   unsigned long long* tstamp;       // profiling record or nullptr
+  unsigned long long* dbg;          // per-CTA phase trace [G][8] (MOEPIC_K2_TRACE) or nullptr
   CombineSeg comb[kMaxLaunchSegs];
 };
 // Partition rule shared with the host: CTA c of G owns launch rows [c*R/G, (c+1)*R/G).

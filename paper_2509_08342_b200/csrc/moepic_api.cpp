@@ -619,7 +619,31 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
     }
     const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
     kp.tstamp = ctx->tstamp(pe);
+    kp.dbg = nullptr;
+    static unsigned long long* dbg_buf = nullptr;   // MOEPIC_K2_TRACE: phase spans to stderr (tools)
+    const bool trace = getenv("MOEPIC_K2_TRACE") != nullptr;
+    if (trace) {
+      if (!dbg_buf) cudaMalloc(&dbg_buf, 148 * 8 * 8);
+      cudaMemsetAsync(dbg_buf, 0, 148 * 8 * 8, s);
+      kp.dbg = dbg_buf;
+    }
     launch_k2(kp, (int)G, tb, s);
+    if (trace) {
+      unsigned long long h[148 * 8];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, dbg_buf, sizeof h, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull, mx[5] = {0, 0, 0, 0, 0}, mn[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+      for (int c = 0; c < G; ++c) t0 = std::min(t0, h[c * 8]);
+      for (int c = 0; c < G; ++c)
+        for (int k = 0; k < 5; ++k)
+          if (h[c * 8 + k]) {
+            mx[k] = std::max(mx[k], h[c * 8 + k] - t0);
+            mn[k] = std::min(mn[k], h[c * 8 + k] - t0);
+          }
+      fprintf(stderr, "[k2trace] G=%lld rows=%lld comb=%d start %llu..%llu first_tile %llu..%llu stream_done %llu..%llu "
+              "barrier %llu..%llu end %llu..%llu ns\n", (long long)G, (long long)R, kp.combine, mn[0], mx[0], mn[1],
+              mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4]);
+    }
     ctx->prof_end(pe, s, alg_bytes);
     CK(cudaGetLastError());
     ++launches;
