@@ -5,7 +5,8 @@
 // of token b are enumerated in a fixed order (segments in step order, chunks in CTA order) and
 // numbered k = 0, 1, ...  A block covers CB consecutive float4 columns of one token; lane l of
 // warp w takes column l % CB and the partials k = w * P + l / CB (mod 16 P), P = 32 / CB, in
-// increasing k; the P lane phases are added by a butterfly, then the 16 warp sums in warp order.
+// increasing k (loads issued four at a time); the P lane phases are added by a butterfly, then
+// the 16 warp sums in warp order.
 // CB (32, 16, 8 or 4) is chosen from the output size only (combine_cb), so small outputs still
 // spread over the whole grid; the order depends only on the step's segment table and the
 // output shape, so the result is deterministic.
@@ -46,32 +47,47 @@ __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, i
   const bool active = c4 < d4;
   const uint32_t bit = 1u << b;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int k0 = 0;   // index of the first chunk of the current segment in token b's list
-  for (int s = 0; s < nsegs; ++s) {
-    const CombineSeg sg = segs[s];
-    if (!(sg.tok_mask & bit)) continue;
-    const int ntok = __popc(sg.tok_mask);
-    const int t = __popc(sg.tok_mask & (bit - 1u));
-    const int64_t stride4 = (int64_t)ntok * d4;
-    const float4* base = reinterpret_cast<const float4*>(ws + sg.ws_off + (int64_t)t * d) + c4;
-    int ci = ((phase - k0) % S + S) % S;        // first chunk with k = phase (mod S)
-    if (active) {
-      for (; ci + 3 * S < sg.nchunks; ci += 4 * S) {   // 4 loads in flight
-        const float4 v0 = base[(int64_t)ci * stride4];
-        const float4 v1 = base[(int64_t)(ci + S) * stride4];
-        const float4 v2 = base[(int64_t)(ci + 2 * S) * stride4];
-        const float4 v3 = base[(int64_t)(ci + 3 * S) * stride4];
-        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+  // flattened walk over token b's partials: a cursor (segment s, its first index k0) moves
+  // forward as k grows, so four addresses are formed before their loads are issued together
+  // (one memory latency per four partials instead of one per segment)
+  int total = 0;
+  for (int s = 0; s < nsegs; ++s)
+    if (segs[s].tok_mask & bit) total += segs[s].nchunks;
+  int cs = 0, ck0 = 0;
+  auto addr = [&](int k) -> const float4* {   // k < total, k non-decreasing across calls
+    for (;;) {
+      const CombineSeg& sg = segs[cs];
+      if ((sg.tok_mask & bit) && k < ck0 + sg.nchunks) {
+        const int ntok = __popc(sg.tok_mask);
+        const int t = __popc(sg.tok_mask & (bit - 1u));
+        return reinterpret_cast<const float4*>(ws + sg.ws_off + (int64_t)t * d) + c4 +
+               (int64_t)(k - ck0) * ntok * d4;
       }
-      for (; ci < sg.nchunks; ci += S) {
-        const float4 v = base[(int64_t)ci * stride4];
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
+      if (sg.tok_mask & bit) ck0 += sg.nchunks;
+      ++cs;
     }
-    k0 += sg.nchunks;
+  };
+  if (active) {
+    int k = phase;
+    for (; k + 3 * S < total; k += 4 * S) {
+      const float4* p0 = addr(k);
+      const float4* p1 = addr(k + S);
+      const float4* p2 = addr(k + 2 * S);
+      const float4* p3 = addr(k + 3 * S);
+      const float4 v0 = *p0, v1 = *p1, v2 = *p2, v3 = *p3;
+      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+      acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+      acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    }
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* q0 = k < total ? addr(k) : nullptr;
+    const float4* q1 = k + S < total ? addr(k + S) : nullptr;
+    const float4* q2 = k + 2 * S < total ? addr(k + 2 * S) : nullptr;
+    const float4 v0 = q0 ? *q0 : z, v1 = q1 ? *q1 : z, v2 = q2 ? *q2 : z;
+    if (q0) { acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w; }
+    if (q1) { acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w; }
+    if (q2) { acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w; }
   }
   // lane phases (lanes CB apart) by a butterfly
   for (int o = CB; o < 32; o <<= 1) {
