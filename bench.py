@@ -132,19 +132,25 @@ def pcie_probe(torch, nbytes=1 << 30, reps=10):
     return best
 
 
-def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print):
+def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print, parallel="ep"):
+    """EP: rank owns experts [rank N/G, (rank+1) N/G).  TP (along I): rank owns rows
+    [rank I/G, (rank+1) I/G) of every expert; budgets are then in units of that slice."""
     S = synth.SHAPES[cfg["shape"]]
     L, Lh = cfg["L"], cfg["L_host"]
-    N_local = S.N // world
+    tp = parallel == "tp" and world > 1
+    N_local = S.N if tp else S.N // world
     v_e = cfg["budget"] * L * N_local
-    desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=64 if S.I % 64 == 0 else 16,
+    I_loc = S.I // world if tp else S.I
+    g = next(x for x in (64, 32, 16) if I_loc % x == 0)
+    desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=g,
                           max_batch=max_batch, renorm_topk=S.renorm, L_host=Lh, v_e_max=v_e,
-                          ep_rank=rank, ep_size=world)
+                          ep_rank=0 if tp else rank, ep_size=1 if tp else world,
+                          tp_rank=rank if tp else 0, tp_size=world if tp else 1)
     t0 = time.time()
     ctx = api.MoEpic(desc)
     for i in range(L):
         ctx.load_router(i, synth.bf16_bits(synth.router_weights(0, i, S.N, S.d)))
-    lo, hi = rank * N_local, (rank + 1) * N_local
+    lo, hi = (0, S.N) if tp else (rank * N_local, (rank + 1) * N_local)
     keep = {}
     for pl in range(Lh):
         for e in range(lo, hi):
@@ -178,7 +184,13 @@ def run_ours(args, log):
     cfg = CONFIGS[args.config]
     pcie = pcie_probe(torch)
     log(f"[bench] pinned H2D probe {pcie:.2f} GB/s")
-    ctx, desc, S, v_e, keep = build_model(api, synth, torch, cfg, rank, world, max_batch=cfg["B"], log=log)
+    parallel = args.parallel
+    if parallel == "auto":   # TP along I for decode (every rank's PCIe link streams every token), EP for prefill
+        parallel = "ep" if cfg.get("prefill") else "tp"
+    if world == 1:
+        parallel = "single"
+    ctx, desc, S, v_e, keep = build_model(api, synth, torch, cfg, rank, world, max_batch=cfg["B"], log=log,
+                                          parallel=parallel)
     L, B = cfg["L"], cfg["B"]
     t0 = time.time()
     base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
@@ -239,7 +251,7 @@ def run_ours(args, log):
                     dist.all_reduce(yc)
                     ylocal.copy_(yc[rank * Bl:(rank + 1) * Bl])
 
-    if world > 1 and cfg.get("prefill"):
+    if parallel == "ep" and cfg.get("prefill"):
         assert B % world == 0, "prefill batch must divide by the EP size"
         step = token_ep_prefill
     else:
@@ -254,7 +266,7 @@ def run_ours(args, log):
         torch.cuda.synchronize()
         k2w = ctx.profile_read(api.M.KERNEL_EXPERT)
         ctx.profile(False)
-        U_e = 6 * S.d * S.I
+        U_e = 6 * S.d * (S.I // world if parallel == "tp" else S.I)   # bytes of one (local) expert
         t_load = U_e / (pcie * 1e9) * 1e3                          # ms per full expert
         t_moe = k2w["total_ms"] / (adapt_tokens * L)               # ms of expert compute per layer-step
         t0 = time.time()
@@ -380,9 +392,11 @@ def run_ours(args, log):
         "dtype": "bf16", "data": "synthetic (seeded random weights, organic routing process; synth/)",
         "config": {"workload": _workload(cfg),
                    "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
-                   "global_batch": B, "seq_len": 1, "parallelism": f"ep{world}" if world > 1 else "single",
+                   "global_batch": B, "seq_len": 1,
+                   "parallelism": f"{parallel}{world}" if world > 1 else "single",
                    "ep_collectives": None if world == 1 else (
-                       "all_gather(h) + reduce_scatter(y), T/G tokens per rank" if prefill else "all_reduce(y)"),
+                       "all_gather(h) + reduce_scatter(y), T/G tokens per rank" if prefill and parallel == "ep"
+                       else "all_reduce(y) of the per-rank partial outputs"),
                    "v_e_experts": base_cfg["v_e"], "theta": base_cfg["theta_i"][0], "mode": args.mode,
                    "policy": MODES[args.mode].get("policy", "LCP"), "prefetch": base_cfg.get("prefetch", True),
                    "y_cap": S.K * B,
@@ -538,6 +552,9 @@ def main():
     ap.add_argument("--mode", default="moepic", choices=sorted(MODES), help="ablation mode (SURVEY §8(f) NEXT-1)")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="time the step without the per-kernel CUDA events (roofline fields then empty)")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "ep", "tp"],
+                    help="N>1 sharding: tp = every expert split along I over the ranks (decode default), "
+                         "ep = experts partitioned over the ranks (prefill default)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (multi-rank test on a 1-GPU box)")
     args = ap.parse_args()

@@ -65,7 +65,7 @@ typedef struct moepic_ctx moepic_ctx;
 /* Model shape (Table 2).  Invariants (EINVAL otherwise):
  *   1 <= K < N; L >= 1; d % 8 == 0 and d >= 8; I % row_granule == 0;
  *   row_granule % 16 == 0; buffer_experts >= K (U_b); 1 <= max_batch <= 4096;
- *   1 <= L_host <= L; 0 <= ep_rank < ep_size; N % ep_size == 0.                               */
+ *   1 <= L_host <= L; 0 <= ep_rank < ep_size; N % ep_size == 0; tp fields as documented below. */
 typedef struct {
   int32_t L, N, K, d, I;  /* layers, routed experts per layer, top-K, hidden, intermediate     */
   int32_t n_shared;       /* shared experts per layer: always resident, weight 1, unsplit (Q6) */
@@ -78,6 +78,18 @@ typedef struct {
   double v_e_max;         /* largest expert-cache budget V_e (full-expert units) configure may
                              request; sizes the HBM slot pool                                  */
   int32_t ep_rank, ep_size; /* expert parallel: expert e is local iff e*ep_size/N == ep_rank   */
+  int32_t tp_rank, tp_size; /* tensor parallel along I (the split identity
+                             P:254 applied across GPUs): this context holds intermediate rows
+                             [tp_rank*I/tp_size, (tp_rank+1)*I/tp_size) of EVERY routed and
+                             shared expert; load_expert takes the full HF tensors and keeps that
+                             slice.  Every size the context reports or accepts (row_granule
+                             multiples, I_top_i, v_e / v_i in full-expert units, byte counters)
+                             refers to the local slice of I/tp_size rows.  Routing is replicated
+                             (bit-identical fp64 logits on every rank), so all ranks take the
+                             same cache decisions.  y_dev is this rank's partial output; the
+                             caller sums it over ranks (all-reduce).  MOEPIC_RESIDUAL adds h on
+                             tp_rank 0 only.  EINVAL unless 0 <= tp_rank < tp_size,
+                             I % (tp_size*row_granule) == 0, and ep_size == 1 when tp_size > 1. */
 } moepic_model_desc;
 
 /* Cache configuration.  EINVAL when: v_e < 0 or

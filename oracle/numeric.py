@@ -164,6 +164,33 @@ def moe_layer_ep_partial(h_bits, router_bits, experts, K, ep_rank, ep_size, shar
     return y
 
 
+def moe_layer_tp_partial(h_bits, router_bits, experts, K, tp_rank, tp_size, shared=(), renorm=True):
+    """Rank tp_rank's share of the layer output under tensor parallelism along I (SURVEY 8(f)
+    NEXT-4): every routed and shared expert restricted to its intermediate rows
+    [r I / G, (r+1) I / G) (gate/up rows, down columns), weighted by the full layer's gate
+    weights.  The split identity of P:254 (a sum of partial down-projections over a partition
+    of I) makes the sum of all ranks' shares equal to moe_layer(...)[0]."""
+    h = bf16_to_f64(h_bits)
+    logits = router_logits(h_bits, router_bits)
+    B, d = h.shape
+    get = experts if callable(experts) else (lambda e: experts[e])
+    y = np.zeros((B, d), dtype=np.float64)
+    for b in range(B):
+        ids = topk_ids(logits[b], K)
+        w = gate_weights(logits[b], ids, renorm)
+        for k, e in enumerate(ids):
+            g, u, dn = (bf16_to_f64(x) for x in get(int(e)))
+            I = g.shape[0]
+            lo, hi = tp_rank * I // tp_size, (tp_rank + 1) * I // tp_size
+            y[b] += w[k] * expert_forward(h[b:b + 1], g[lo:hi], u[lo:hi], dn[:, lo:hi])[0]
+    for (gate, up, down) in shared:
+        g, u, dn = bf16_to_f64(gate), bf16_to_f64(up), bf16_to_f64(down)
+        I = g.shape[0]
+        lo, hi = tp_rank * I // tp_size, (tp_rank + 1) * I // tp_size
+        y += expert_forward(h, g[lo:hi], u[lo:hi], dn[:, lo:hi])
+    return y
+
+
 def predicted_ranking(pred_logits: np.ndarray, K: int) -> np.ndarray:
     """Next-layer ranking R' of all N experts (Eq. 3; reading Q9).
 

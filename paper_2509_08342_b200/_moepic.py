@@ -34,7 +34,8 @@ class moepic_model_desc(C.Structure):
     _fields_ = [("L", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("d", C.c_int32), ("I", C.c_int32),
                 ("n_shared", C.c_int32), ("row_granule", C.c_int32), ("buffer_experts", C.c_int32),
                 ("max_batch", C.c_int32), ("renorm_topk", C.c_int32), ("L_host", C.c_int32),
-                ("v_e_max", C.c_double), ("ep_rank", C.c_int32), ("ep_size", C.c_int32)]
+                ("v_e_max", C.c_double), ("ep_rank", C.c_int32), ("ep_size", C.c_int32),
+                ("tp_rank", C.c_int32), ("tp_size", C.c_int32)]
 
 
 class moepic_cache_config(C.Structure):

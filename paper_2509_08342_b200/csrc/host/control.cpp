@@ -1,4 +1,5 @@
 // Host control plane implementation — see control.hpp.  Compiled with -ffp-contract=off.
+#include <cstdlib>
 #include "control.hpp"
 
 #include <algorithm>
@@ -426,7 +427,7 @@ void ControlPlane::make_plan(int j, const int32_t* ranking, Plan& out) const {
   const LayerState& l = layers[j];
   const int64_t cap_rows = (int64_t)U_b * I;
   int ycap = cfg.y_cap.empty() ? N : cfg.y_cap[j];
-  if (l.Y >= 0) ycap = std::min(ycap, l.Y);
+  if (l.Y >= 0 && !getenv("MOEPIC_NO_SOLVER_YCAP")) ycap = std::min(ycap, l.Y);   // env: experiments
   int64_t used = 0;
   for (int y = 0; y < N; ++y) {
     int e = ranking[y];

@@ -65,7 +65,23 @@ std::string validate_desc(const moepic_model_desc* d) {
   if (!(d->v_e_max >= 0.0)) return "v_e_max must be >= 0";
   if (d->ep_size < 1 || d->ep_rank < 0 || d->ep_rank >= d->ep_size) return "ep_rank / ep_size invalid";
   if (d->N % d->ep_size != 0) return "N must be divisible by ep_size";
+  if (d->tp_size < 1 || d->tp_rank < 0 || d->tp_rank >= d->tp_size) return "tp_rank / tp_size invalid";
+  if (d->tp_size > 1 && d->ep_size != 1) return "tp_size > 1 needs ep_size == 1";
+  if (d->I % ((int64_t)d->tp_size * d->row_granule) != 0) return "I must be a multiple of tp_size * row_granule";
   return "";
+}
+
+// The context works on its tensor-parallel slice: I/tp_size rows of every expert (SURVEY
+// §8(f) NEXT-4).  Everything below create / hostsim_create sees this local shape.
+moepic_model_desc local_desc(const moepic_model_desc& d) {
+  moepic_model_desc l = d;
+  l.I = d.I / d.tp_size;
+  return l;
+}
+
+// h is added to y by exactly one rank when the output is a sum over ranks (EP and TP)
+inline bool adds_residual(const moepic_model_desc& d, uint32_t flags) {
+  return (flags & MOEPIC_RESIDUAL) && d.ep_rank == 0 && d.tp_rank == 0;
 }
 
 ArenaLayout arena_layout(const moepic_model_desc& d) {
@@ -199,7 +215,8 @@ struct moepic_ctx {
   std::unique_ptr<PfPermuteParams> pf_pp = std::make_unique<PfPermuteParams>();
   std::unique_ptr<PfGemmParams> pf_gp = std::make_unique<PfGemmParams>();
   std::unique_ptr<CombineParams> cpar = std::make_unique<CombineParams>();
-  moepic_model_desc desc{};
+  moepic_model_desc desc{};         // local shape: desc.I = I_full / tp_size rows per expert
+  int32_t I_full = 0;               // rows per expert in the caller's (HF) tensors
   ArenaLayout lay{};
   std::unique_ptr<ControlPlane> cp;
   uint8_t* arena = nullptr;
@@ -234,8 +251,8 @@ struct moepic_ctx {
     size_t bytes;
     int32_t item;
   };
-  static constexpr size_t kFeedChunk = 8ull << 20;
-  static constexpr size_t kFeedDepth = 3;
+  size_t kFeedChunk = 8ull << 20;
+  size_t kFeedDepth = 3;
   static constexpr int kFeedRing = 16;
   bool cancel_prefetch = true;
   std::vector<FeedChunk> feed;
@@ -372,7 +389,7 @@ extern "C" {
 
 moepic_status moepic_arena_bytes(const moepic_model_desc* desc, size_t* bytes) {
   if (!bytes || !validate_desc(desc).empty()) return MOEPIC_EINVAL;
-  *bytes = arena_layout(*desc).total;
+  *bytes = arena_layout(local_desc(*desc)).total;
   return MOEPIC_OK;
 }
 
@@ -382,11 +399,15 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   *out = nullptr;
   if (!validate_desc(desc).empty()) return MOEPIC_EINVAL;
   if (!dev_arena || (reinterpret_cast<uintptr_t>(dev_arena) % kAlign) != 0) return MOEPIC_EINVAL;
+  const moepic_model_desc full = *desc;
+  const moepic_model_desc local = local_desc(full);
+  desc = &local;
   ArenaLayout lay = arena_layout(*desc);
   if (dev_bytes < lay.total) return MOEPIC_ENOMEM;
   auto* ctx = new (std::nothrow) moepic_ctx();
   if (!ctx) return MOEPIC_ENOMEM;
   ctx->desc = *desc;
+  ctx->I_full = full.I;
   ctx->lay = lay;
   ctx->arena = static_cast<uint8_t*>(dev_arena);
   ctx->cp.reset(new ControlPlane(desc->L, desc->N, desc->K, desc->d, desc->I, desc->row_granule,
@@ -422,6 +443,8 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (cudaMemset(ctx->arena + lay.ticket, 0, 64) != cudaSuccess ||
       cudaMemset(ctx->arena + lay.rsel, 0, (size_t)desc->N * 16) != cudaSuccess)
     return bail(MOEPIC_ERUNTIME);
+  if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;   // experiments
+  if (const char* e = getenv("MOEPIC_FEED_DEPTH")) ctx->kFeedDepth = (size_t)atol(e);
   ctx->slot_base.assign(desc->L, 0);
   ctx->ids_h.resize((size_t)desc->max_batch * desc->K);
   ctx->w_h.resize((size_t)desc->max_batch * desc->K);
@@ -439,9 +462,13 @@ moepic_status moepic_load_router(moepic_ctx* ctx, int32_t layer, const uint16_t*
   return MOEPIC_OK;
 }
 
-// HF layout -> row-interleaved rows [gate_r | up_r | down[:, r]]
+// HF layout -> row-interleaved rows [gate_r | up_r | down[:, r]] for r in [r0, r0 + I); the HF
+// tensors hold I_full rows (gate/up [I_full][d], down [d][I_full]); r0 = tp_rank * I.
 static void pack_rows(uint8_t* dst, const uint16_t* gate, const uint16_t* up, const uint16_t* down, int d,
-                      int I) {
+                      int I, int r0, int I_full) {
+  gate += (size_t)r0 * d;
+  up += (size_t)r0 * d;
+  down += r0;
   const size_t rowe = 3ull * d;
   uint16_t* o = reinterpret_cast<uint16_t*>(dst);
 #pragma omp parallel for schedule(static)
@@ -455,7 +482,7 @@ static void pack_rows(uint8_t* dst, const uint16_t* gate, const uint16_t* up, co
       const int ke = std::min(d, k0 + 64);
       for (int r = rb; r < re; ++r) {
         uint16_t* orow = o + (size_t)r * rowe + 2 * d;
-        for (int k = k0; k < ke; ++k) orow[k] = down[(size_t)k * I + r];
+        for (int k = k0; k < ke; ++k) orow[k] = down[(size_t)k * I_full + r];
       }
     }
   }
@@ -470,14 +497,15 @@ moepic_status moepic_load_expert(moepic_ctx* ctx, int32_t layer, int32_t expert,
     if (expert >= d.N) return fail(&ctx->err, MOEPIC_EINVAL, "expert out of range");
     if (layer < 0 || layer >= d.L_host) return fail(&ctx->err, MOEPIC_EINVAL, "layer must be < L_host");
     if (!ctx->cp->is_local(expert)) return MOEPIC_OK;   // another EP rank owns it
-    pack_rows(const_cast<uint8_t*>(ctx->host_expert(layer, expert)), gate, up, down, d.d, d.I);
+    pack_rows(const_cast<uint8_t*>(ctx->host_expert(layer, expert)), gate, up, down, d.d, d.I,
+              d.tp_rank * d.I, ctx->I_full);
     return MOEPIC_OK;
   }
   const int s = -1 - expert;
   if (s >= d.n_shared) return fail(&ctx->err, MOEPIC_EINVAL, "shared expert index out of range");
   if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
   std::vector<uint8_t> tmp((size_t)d.I * ctx->rb());
-  pack_rows(tmp.data(), gate, up, down, d.d, d.I);
+  pack_rows(tmp.data(), gate, up, down, d.d, d.I, d.tp_rank * d.I, ctx->I_full);
   CK(cudaMemcpy(ctx->shared_ptr(layer, s), tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
   return MOEPIC_OK;
 }
@@ -667,7 +695,7 @@ static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s, size_t w0, si
 #if defined(__x86_64__)
     __builtin_ia32_pause();
 #endif
-    if ((spins & 0x3F) == 0 && !ctx->feed_pump(moepic_ctx::kFeedDepth)) {
+    if ((spins & 0x3F) == 0 && !ctx->feed_pump(ctx->kFeedDepth)) {
       ctx->poisoned = true;
       return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch feed: %s", cudaGetErrorString(cudaGetLastError()));
     }
@@ -770,11 +798,11 @@ static moepic_status issue_plan(moepic_ctx* ctx, Plan& plan, int buf) {
     const uint8_t* src = ctx->host_expert(j, it.expert) + (it.full ? 0 : (uint64_t)l.I_top * rb);
     uint8_t* dst = ctx->plan_ptr(buf, it.buf_row);
     const size_t total = (size_t)it.rows * rb;
-    for (size_t off = 0; off < total; off += moepic_ctx::kFeedChunk)
-      ctx->feed.push_back({dst + off, src + off, std::min(moepic_ctx::kFeedChunk, total - off), (int32_t)k});
+    for (size_t off = 0; off < total; off += ctx->kFeedChunk)
+      ctx->feed.push_back({dst + off, src + off, std::min(ctx->kFeedChunk, total - off), (int32_t)k});
   }
   ctx->ctr.pcie_prefetch_planned_bytes += plan_bytes(plan, (int64_t)rb);
-  if (!ctx->feed_pump(ctx->cancel_prefetch ? moepic_ctx::kFeedDepth : (size_t)-1)) {
+  if (!ctx->feed_pump(ctx->cancel_prefetch ? ctx->kFeedDepth : (size_t)-1)) {
     ctx->poisoned = true;
     return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch copy: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -959,7 +987,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   cp2.y = y; cp2.h = h; cp2.Y = Y; cp2.pos = pos;
   cp2.w = reinterpret_cast<const float*>(ctx->arena + ctx->lay.w);
   cp2.T = T; cp2.K = K; cp2.d = d.d; cp2.n_shared = NS;
-  cp2.residual = ((flags & MOEPIC_RESIDUAL) && d.ep_rank == 0) ? 1 : 0;
+  cp2.residual = adds_residual(d, flags) ? 1 : 0;
   for (int s2 = 0; s2 < NS; ++s2) cp2.shared_off[s2] = moff[N + s2];
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_COMBINE);
   launch_pf_combine(cp2, s);
@@ -1093,7 +1121,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   // ---- K2 launches: resident now / prefetched / on-demand, then the combine
   int64_t ws_next = 0;
   std::vector<CombineSeg> comb;
-  FuseCombine fuse{y_dev, ((flags & MOEPIC_RESIDUAL) && d.ep_rank == 0) ? 1 : 0, false};
+  FuseCombine fuse{y_dev, adds_residual(d, flags) ? 1 : 0, false};
   const bool lastA = gB.empty() && gC.empty(), lastB = gC.empty();
   st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches, lastA ? &fuse : nullptr);
   if (st != MOEPIC_OK) return st;
@@ -1115,7 +1143,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   cpar.ws = reinterpret_cast<const float*>(ctx->arena + ctx->lay.ws);
   cpar.B = B;
   cpar.d = d.d;
-  cpar.residual = ((flags & MOEPIC_RESIDUAL) && d.ep_rank == 0) ? 1 : 0;   // h added once across ranks
+  cpar.residual = adds_residual(d, flags) ? 1 : 0;   // h added once across ranks
   cpar.nsegs = (int)comb.size();
   for (size_t i = 0; i < comb.size(); ++i) cpar.segs[i] = comb[i];
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_COMBINE);
@@ -1348,6 +1376,8 @@ moepic_status moepic_hostsim_create(const moepic_model_desc* desc, moepic_hostsi
   if (!validate_desc(desc).empty()) return MOEPIC_EINVAL;
   auto* hs = new (std::nothrow) moepic_hostsim();
   if (!hs) return MOEPIC_ENOMEM;
+  const moepic_model_desc local = local_desc(*desc);
+  desc = &local;
   hs->desc = *desc;
   hs->lay = arena_layout(*desc);
   hs->cp.reset(new ControlPlane(desc->L, desc->N, desc->K, desc->d, desc->I, desc->row_granule,

@@ -42,9 +42,18 @@ def test_arena_bytes_and_desc_validation():
     assert M.moepic_arena_bytes(ctypes.byref(d), ctypes.byref(n)) == M.OK
     # slot pool of 128 experts (45 GB) + 2 ping-pong halves of 4 experts
     assert n.value > 128 * 352321536 + 2 * 4 * 352321536
-    for bad in (dict(K=8), dict(d=4100), dict(I=1000), dict(max_batch=8192), dict(L_host=40)):
+    # tensor parallel along I: the arena holds the local slice of I / tp_size rows per expert
+    nt = ctypes.c_size_t()
+    dt = api.model_desc(32, 8, 2, 4096, 14336, max_batch=1, v_e_max=128, L_host=2, tp_rank=1, tp_size=4)
+    assert M.moepic_arena_bytes(ctypes.byref(dt), ctypes.byref(nt)) == M.OK
+    assert 128 * 352321536 // 4 < nt.value < n.value // 3
+    for bad in (dict(K=8), dict(d=4100), dict(I=1000), dict(max_batch=8192), dict(L_host=40),
+                dict(tp_size=0), dict(tp_rank=2, tp_size=2), dict(tp_size=3),
+                dict(tp_size=2, ep_size=2), dict(I=14336 + 64, tp_size=2)):
         kw = dict(L=32, N=8, K=2, d=4096, I=14336, max_batch=1, v_e_max=128, L_host=2)
         kw.update(bad)
+        if "I" in bad and "tp_size" in bad:   # I = 14400 = 225 granules: odd, so no even split
+            kw["row_granule"] = 64
         d = api.model_desc(**kw)
         assert M.moepic_arena_bytes(ctypes.byref(d), ctypes.byref(n)) == M.EINVAL
 

@@ -160,9 +160,9 @@ def test_moe_layer_matches_hf_qwen3_block(norm):
     np.testing.assert_allclose(y, ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
 
 
-def test_moe_layer_matches_hf_deepseek_v2_block():
-    """Renorm off + 2 shared experts; HF's single shared MLP of 2I rows equals our two
-    shared experts of I rows by the split identity (reading Q6)."""
+def _deepseek_hf_case():
+    """Renorm off + 2 shared experts through HF's DeepseekV2Moe in fp64; HF's single shared MLP
+    of 2I rows equals our two shared experts of I rows by the split identity (reading Q6)."""
     from transformers import DeepseekV2Config
     from transformers.models.deepseek_v2.modeling_deepseek_v2 import DeepseekV2Moe
     N, d, I, K = 16, 64, 32, 3
@@ -184,8 +184,26 @@ def test_moe_layer_matches_hf_deepseek_v2_block():
         blk.shared_experts.up_proj.weight.copy_(torch.cat([f(shared[0][1]), f(shared[1][1])], 0))
         blk.shared_experts.down_proj.weight.copy_(torch.cat([f(shared[0][2]), f(shared[1][2])], 1))
         ref = blk(f(h)[None]).squeeze(0).numpy()
+    return h, router, experts, shared, K, ref
+
+
+def test_moe_layer_matches_hf_deepseek_v2_block():
+    h, router, experts, shared, K, ref = _deepseek_hf_case()
     y, _, _, _ = O.moe_layer(h, router, experts, K=K, shared=shared, renorm=False)
     np.testing.assert_allclose(y, ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_tp_partials_sum_to_hf_block(G):
+    """C-P16 for tensor parallelism along I: the per-rank shares over the
+    row partition {[rI/G, (r+1)I/G)} of every routed and shared expert sum to HF's
+    DeepseekV2Moe output; each share alone is NOT the full output (a dropped slice would show)."""
+    h, router, experts, shared, K, ref = _deepseek_hf_case()
+    parts = [O.moe_layer_tp_partial(h, router, experts, K, r, G, shared=shared, renorm=False) for r in range(G)]
+    y = np.sum(parts, axis=0)
+    np.testing.assert_allclose(y, ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
+    for p in parts:
+        assert np.abs(p - ref).max() > 1e-3 * np.abs(ref).max()
 
 
 def test_single_expert_reduces_to_plain_mlp():
