@@ -43,6 +43,7 @@ struct RouterParams {
   int32_t* sel_cnt;                 // [N] zero-initialised, reset by k1_select
   unsigned long long* sel_max;      // [N] order-preserving max-logit keys, reset to 0
   unsigned long long* tstamp;       // profiling record (device_utils.cuh) or nullptr
+  unsigned long long* dbg;          // MOEPIC_K1_TRACE phase stamps [8] (tools) or nullptr
 };
 constexpr int kRouterSplitB = 32;
 constexpr int kProfRing = 4096;   // profiling records (events + in-kernel timestamps) per drain

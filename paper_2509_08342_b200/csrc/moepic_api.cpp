@@ -287,6 +287,8 @@ struct moepic_ctx {
     feed_cancel.clear();
   }
 
+  unsigned long long* k1dbg = nullptr;   // MOEPIC_K1_TRACE ring (tools)
+  uint64_t k1dbg_n = 0;
   bool profiling = false;
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
@@ -750,6 +752,17 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   rp.B = B; rp.d = d.d; rp.N = d.N; rp.K = d.K; rp.renorm = d.renorm_topk;
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_ROUTER);
   rp.tstamp = ctx->tstamp(pe);
+  rp.dbg = nullptr;
+  if (getenv("MOEPIC_K1_TRACE")) {   // phase stamps per launch (tools): ring of 4096 x 8 u64
+    if (!ctx->k1dbg) {
+      cudaMalloc(&ctx->k1dbg, 4096 * 64);
+      cudaMemset(ctx->k1dbg, 0, 4096 * 64);
+    }
+    rp.dbg = ctx->k1dbg + (ctx->k1dbg_n % 4096) * 8;
+    cudaMemsetAsync(rp.dbg, 0xFF, 8, s);
+    cudaMemsetAsync(rp.dbg + 1, 0, 56, s);
+    ctx->k1dbg_n++;
+  }
   launch_router(rp, s);
   ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
   CK(cudaGetLastError());
@@ -1345,6 +1358,24 @@ const char* moepic_last_error(const moepic_ctx* ctx) { return ctx ? ctx->err.c_s
 void moepic_destroy(moepic_ctx* ctx) {
   if (!ctx) return;
   cudaDeviceSynchronize();
+  if (ctx->k1dbg) {   // MOEPIC_K1_TRACE summary: mean phase offsets from the first CTA start (us)
+    std::vector<unsigned long long> h(4096 * 8);
+    cudaMemcpy(h.data(), ctx->k1dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    const size_t n = std::min<uint64_t>(ctx->k1dbg_n, 4096);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    size_t cnt = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const unsigned long long* r = &h[i * 8];
+      if (r[0] == ~0ull || r[4] < r[0] || r[3] < r[0]) continue;
+      for (int k = 1; k < 8; ++k) acc[k] += r[k] >= r[0] && r[k] != ~0ull ? (double)(r[k] - r[0]) * 1e-3 : 0.0;
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr, "[k1trace] %zu launches: phase1_end %.2f select_start %.2f selected %.2f routed %.2f "
+              "pred_topk %.2f ranked %.2f end %.2f us\n", cnt, acc[1] / cnt, acc[2] / cnt, acc[5] / cnt,
+              acc[3] / cnt, acc[6] / cnt, acc[7] / cnt, acc[4] / cnt);
+    cudaFree(ctx->k1dbg);
+  }
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   for (auto e : ctx->feed_ev)
     if (e) cudaEventDestroy(e);
