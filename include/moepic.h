@@ -90,7 +90,17 @@ typedef struct {
                              caller sums it over ranks (all-reduce).  MOEPIC_RESIDUAL adds h on
                              tp_rank 0 only.  EINVAL unless 0 <= tp_rank < tp_size,
                              I % (tp_size*row_granule) == 0, and ep_size == 1 when tp_size > 1. */
+  int32_t weight_format;  /* MOEPIC_BF16 (0): experts stored and streamed as bf16.
+                             MOEPIC_Q4G64 (1): low-bit experts (the paper's
+                             Mixtral ran HQQ low-bit experts): load_expert quantises
+                             every stored row vector (gate row, up row, down column) in groups
+                             of 64 to 4-bit codes with a bf16 scale and minimum (DESIGN.md
+                             reading Q28); K2 dequantises on the fly (fp32 accumulation).  A
+                             row then takes 27d/16 bytes (padded to 16) instead of 6d, so every
+                             PCIe and HBM byte count shrinks ~3.5x.  Needs d % 64 == 0 and
+                             max_batch <= 32 (decode; the tcgen05 prefill GEMMs are bf16).     */
 } moepic_model_desc;
+enum { MOEPIC_BF16 = 0, MOEPIC_Q4G64 = 1 };
 
 /* Cache configuration.  EINVAL when: v_e < 0 or
  * v_e > v_e_max; any theta_i outside (0, 1]; any v_i < 0; sum v_i > v_e (+1e-9); policy out
@@ -157,6 +167,13 @@ moepic_status moepic_arena_bytes(const moepic_model_desc* desc, size_t* bytes);
  * events.  On success *out is a new context; on failure *out is NULL.                         */
 moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size_t dev_bytes,
                             moepic_ctx** out);
+
+/* Host-only (no context, no GPU): the pinned-arena image of one expert as load_expert stores
+ * it — this rank's I/tp_size interleaved rows in desc->weight_format (bf16: 6d bytes per row;
+ * Q4G64: codes + group parameters).  out must hold *bytes = rows x row bytes;
+ * out == NULL queries that size.  Lets tests compare the quantiser with the oracle bit for bit. */
+moepic_status moepic_pack_expert(const moepic_model_desc* desc, const uint16_t* gate, const uint16_t* up,
+                                 const uint16_t* down, void* out, size_t* bytes);
 
 /* Router R^layer: w_bf16 host pointer to [N][d] bf16 (row j = expert j), copied.  layer < L. */
 moepic_status moepic_load_router(moepic_ctx* ctx, int32_t layer, const uint16_t* w_bf16);

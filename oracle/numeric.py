@@ -20,6 +20,14 @@ __all__ = [
 ]
 
 
+def weights_f64(w: np.ndarray) -> np.ndarray:
+    """Expert weights as fp64: uint16 arrays are bf16 bit patterns; float64 arrays (dequantised
+    low-bit experts, oracle/quant.py) are taken as they are."""
+    if np.asarray(w).dtype == np.float64:
+        return np.asarray(w)
+    return bf16_to_f64(w)
+
+
 def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
     """uint16 bf16 bit patterns -> exact fp64 values."""
     b = np.ascontiguousarray(bits, dtype=np.uint16)
@@ -126,14 +134,14 @@ def moe_layer(h_bits, router_bits, experts, K, shared=(), renorm=True):
     w = np.stack([gate_weights(logits[b], ids[b], renorm) for b in range(B)])
     y = np.zeros((B, d), dtype=np.float64)
     for e in sorted(set(ids.ravel().tolist())):
-        gate, up, down = (bf16_to_f64(x) for x in get(e))
+        gate, up, down = (weights_f64(x) for x in get(e))
         rows = [b for b in range(B) if e in ids[b]]
         out = expert_forward(h[rows], gate, up, down)
         for r, b in enumerate(rows):
             k = int(np.where(ids[b] == e)[0][0])
             y[b] += w[b, k] * out[r]
     for (gate, up, down) in shared:
-        y += expert_forward(h, bf16_to_f64(gate), bf16_to_f64(up), bf16_to_f64(down))
+        y += expert_forward(h, weights_f64(gate), weights_f64(up), weights_f64(down))
     return y, ids, w, logits
 
 

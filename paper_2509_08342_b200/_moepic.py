@@ -22,6 +22,7 @@ LCP, LRU, LFU, RND = 0, 1, 2, 3
 ALPHA, BETA, GAMMA = 0, 1, 2
 ADM_FREE_SLOT, ADM_NONE = -1, -2
 FUSE_PREDICT, RESIDUAL = 1, 2
+BF16, Q4G64 = 0, 1
 
 _i32p = C.POINTER(C.c_int32)
 _f32p = C.POINTER(C.c_float)
@@ -35,7 +36,7 @@ class moepic_model_desc(C.Structure):
                 ("n_shared", C.c_int32), ("row_granule", C.c_int32), ("buffer_experts", C.c_int32),
                 ("max_batch", C.c_int32), ("renorm_topk", C.c_int32), ("L_host", C.c_int32),
                 ("v_e_max", C.c_double), ("ep_rank", C.c_int32), ("ep_size", C.c_int32),
-                ("tp_rank", C.c_int32), ("tp_size", C.c_int32)]
+                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("weight_format", C.c_int32)]
 
 
 class moepic_cache_config(C.Structure):
@@ -78,6 +79,8 @@ _ctxp = C.c_void_p
 _sig = {
     "moepic_arena_bytes": (C.c_int, [C.POINTER(moepic_model_desc), C.POINTER(C.c_size_t)]),
     "moepic_create": (C.c_int, [C.POINTER(moepic_model_desc), C.c_void_p, C.c_size_t, C.POINTER(_ctxp)]),
+    "moepic_pack_expert": (C.c_int, [C.POINTER(moepic_model_desc), _u16p, _u16p, _u16p, C.c_void_p,
+                                     C.POINTER(C.c_size_t)]),
     "moepic_load_router": (C.c_int, [_ctxp, C.c_int32, _u16p]),
     "moepic_load_expert": (C.c_int, [_ctxp, C.c_int32, C.c_int32, _u16p, _u16p, _u16p]),
     "moepic_configure": (C.c_int, [_ctxp, C.POINTER(moepic_cache_config), C.POINTER(moepic_config_out)]),

@@ -28,16 +28,33 @@ def _ptr(a, t):
 
 
 def model_desc(L, N, K, d, I, n_shared=0, row_granule=64, buffer_experts=None, max_batch=1,
-               renorm_topk=1, L_host=None, v_e_max=None, ep_rank=0, ep_size=1, tp_rank=0, tp_size=1):
+               renorm_topk=1, L_host=None, v_e_max=None, ep_rank=0, ep_size=1, tp_rank=0, tp_size=1,
+               weight_format=0):
     """Model shape (include/moepic.h moepic_model_desc).  With tp_size > 1 the context holds rows
     [tp_rank*I/tp_size, (tp_rank+1)*I/tp_size) of every expert; v_e_max is then in units of that
-    local slice, and load_expert still takes the full HF tensors."""
+    local slice, and load_expert still takes the full HF tensors.  weight_format = M.Q4G64 stores
+    the experts as 4-bit group-quantised rows (include/moepic.h)."""
     return M.moepic_model_desc(L=L, N=N, K=K, d=d, I=I, n_shared=n_shared, row_granule=row_granule,
                                buffer_experts=K if buffer_experts is None else buffer_experts,
                                max_batch=max_batch, renorm_topk=renorm_topk,
                                L_host=L if L_host is None else L_host,
                                v_e_max=float(L * N if v_e_max is None else v_e_max),
-                               ep_rank=ep_rank, ep_size=ep_size, tp_rank=tp_rank, tp_size=tp_size)
+                               ep_rank=ep_rank, ep_size=ep_size, tp_rank=tp_rank, tp_size=tp_size,
+                               weight_format=weight_format)
+
+
+def pack_expert(desc, gate_bits, up_bits, down_bits) -> np.ndarray:
+    """moepic_pack_expert: the library's stored image of one expert ([rows][row bytes] uint8)."""
+    g = np.ascontiguousarray(gate_bits, dtype=np.uint16)
+    u = np.ascontiguousarray(up_bits, dtype=np.uint16)
+    dn = np.ascontiguousarray(down_bits, dtype=np.uint16)
+    n = C.c_size_t()
+    _check(M.moepic_pack_expert(C.byref(desc), _ptr(g, C.c_uint16), _ptr(u, C.c_uint16), _ptr(dn, C.c_uint16),
+                                None, C.byref(n)), "moepic_pack_expert")
+    out = np.zeros(n.value, np.uint8)
+    _check(M.moepic_pack_expert(C.byref(desc), _ptr(g, C.c_uint16), _ptr(u, C.c_uint16), _ptr(dn, C.c_uint16),
+                                out.ctypes.data_as(C.c_void_p), C.byref(n)), "moepic_pack_expert")
+    return out
 
 
 class _Cfg:

@@ -43,30 +43,33 @@ struct Tile {
 
 }  // namespace
 
-int k2_rows_per_tile(int d) {
-  if (d > 2048) return 2;
-  if (d > 1024) return 4;
-  if (d > 512) return 8;
-  return 16;
+// Q4G64 rows: [gate | up | down codes, d/2 bytes each][3 x d/64 (scale, min)
+// bf16 pairs], padded to 16 bytes; ~3.5x smaller than bf16 rows, so tiles hold twice the rows
+__host__ __device__ inline int k2_row_bytes(int d, int q4) {
+  return q4 ? (3 * (d / 2) + 3 * (d / 64) * 4 + 15) / 16 * 16 : 6 * d;
+}
+int k2_rows_per_tile(int d, int q4) {
+  const int rs = d > 2048 ? 2 : d > 1024 ? 4 : d > 512 ? 8 : 16;
+  return q4 ? (rs * 2 > 16 ? 16 : rs * 2) : rs;
 }
 static int k2_cw(int d) { return d > 2048 ? 8 : 4; }
-int k2_max_tokens(int d) {   // 2 * RS * TB <= 32 reduced values per tile
-  const int rs = k2_rows_per_tile(d);
+int k2_max_tokens(int d, int q4) {   // 2 * RS * TB <= 32 reduced values per tile
+  const int rs = k2_rows_per_tile(d, q4);
   return rs <= 4 ? 4 : 16 / rs;
 }
-size_t k2_smem_bytes(int d) {
-  const int RS = k2_rows_per_tile(d);
-  return (size_t)kStagesV2 * RS * 6 * d + (2 * kStagesV2 + 2) * sizeof(uint64_t) +
+size_t k2_smem_bytes(int d, int q4) {
+  const int RS = k2_rows_per_tile(d, q4);
+  return (size_t)kStagesV2 * RS * k2_row_bytes(d, q4) + (2 * kStagesV2 + 2) * sizeof(uint64_t) +
          (size_t)2 * kConsumerWarps * 32 * sizeof(float) + 128;
 }
 
-template <int TB, int CW, int RS, class P>
+template <int TB, int CW, int RS, int Q4, class P>
 __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_constant__ P p) {
   static_assert(2 * RS * TB <= 32, "one lane per reduced value");
   constexpr int NV = 2 * RS * TB;
   extern __shared__ __align__(128) uint8_t smem[];
   const int d = p.d;
-  const int rowb = 6 * d;
+  const int rowb = k2_row_bytes(d, Q4);
   const int tileb = RS * rowb;
   uint8_t* stages = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStagesV2 * tileb);
@@ -146,9 +149,25 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   const uint8_t* prev_tile = nullptr;
   int prev_stage = -1;
 
-  auto load_row = [&](const uint8_t* base, float* f) {
-    if constexpr (CW == 8) unpack8(*reinterpret_cast<const uint4*>(base + c0 * 2), f);
-    else unpack4(*reinterpret_cast<const uint2*>(base + c0 * 2), f);
+  // the thread's CW weights of part (0 gate, 1 up, 2 down) of a stored row, as fp32
+  auto load_part = [&](const uint8_t* row, int part, float* f) {
+    if constexpr (Q4 == 0) {
+      const uint8_t* base = row + (size_t)part * 2 * d;
+      if constexpr (CW == 8) unpack8(*reinterpret_cast<const uint4*>(base + c0 * 2), f);
+      else unpack4(*reinterpret_cast<const uint2*>(base + c0 * 2), f);
+    } else {   // x = min + code * scale; code -> float exactly via the 2^23 magic constant
+      const uint32_t prm =
+          *reinterpret_cast<const uint32_t*>(row + 3 * (d / 2) + (part * (d >> 6) + (c0 >> 6)) * 4);
+      const float sc = __uint_as_float(prm << 16), mn = __uint_as_float(prm & 0xFFFF0000u);
+      uint32_t c;
+      if constexpr (CW == 8) c = *reinterpret_cast<const uint32_t*>(row + part * (d / 2) + (c0 >> 1));
+      else c = *reinterpret_cast<const uint16_t*>(row + part * (d / 2) + (c0 >> 1));
+#pragma unroll
+      for (int i = 0; i < CW; ++i) {
+        const float q = __uint_as_float(0x4B000000u | ((c >> (4 * i)) & 15u)) - 8388608.0f;
+        f[i] = fmaf(q, sc, mn);
+      }
+    }
   };
   auto flush = [&](int s, int nt) {
     const Seg& sg = p.segs[s];
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     for (int r = 0; r < RS; ++r) {
       if (r < prev_nr) {
         float dn[CW];
-        load_row(prev_tile + (size_t)r * rowb + 4 * d, dn);
+        load_part(prev_tile + (size_t)r * rowb, 2, dn);
 #pragma unroll
         for (int t = 0; t < TB; ++t) {
           const float a = act_prev[r][t];
@@ -235,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       for (int r = 0; r < RS; ++r) {
         if (r < nr) {
           float g[CW], u[CW];
-          load_row(tile + (size_t)r * rowb, g);
-          load_row(tile + (size_t)r * rowb + 2 * d, u);
+          load_part(tile + (size_t)r * rowb, 0, g);
+          load_part(tile + (size_t)r * rowb, 1, u);
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
             if constexpr (TB <= 2) {   // FFMA2 needs the odd partials: only where registers allow
@@ -387,7 +406,7 @@ struct K2ParamsCap {
   CombineSeg comb[CAP];
 };
 
-template <int TB, int CW, int RS, int CAP>
+template <int TB, int CW, int RS, int Q4, int CAP>
 static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   K2ParamsCap<CAP> q;
   q.h = p.h; q.ids = p.ids; q.w = p.w; q.ws = p.ws; q.total_rows = p.total_rows;
@@ -396,52 +415,61 @@ static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0;
   q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target; q.tstamp = p.tstamp; q.dbg = p.dbg;
   for (int i = 0; i < q.ncomb; ++i) q.comb[i] = p.comb[i];
-  auto* fn = k2_split_expert<TB, CW, RS, K2ParamsCap<CAP>>;
+  auto* fn = k2_split_expert<TB, CW, RS, Q4, K2ParamsCap<CAP>>;
+  const size_t smem = k2_smem_bytes(p.d, Q4);
   if (p.combine) {   // grid barrier: every CTA must be co-resident
     void* args[] = {&q};
-    cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, k2_smem_bytes(p.d), s);
+    cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, smem, s);
   } else {
-    fn<<<grid, kThreads, k2_smem_bytes(p.d), s>>>(q);
+    fn<<<grid, kThreads, smem, s>>>(q);
   }
 }
 
-template <int TB, int CW, int RS>
+template <int TB, int CW, int RS, int Q4>
 static void k2_launch_cap(const K2Params& p, int grid, cudaStream_t s) {
   const int n = p.combine && p.ncomb > p.nsegs ? p.ncomb : p.nsegs;
-  if (n <= 8) k2_launch_t<TB, CW, RS, 8>(p, grid, s);
-  else if (n <= 32) k2_launch_t<TB, CW, RS, 32>(p, grid, s);
-  else k2_launch_t<TB, CW, RS, kMaxLaunchSegs>(p, grid, s);
+  if (n <= 8) k2_launch_t<TB, CW, RS, Q4, 8>(p, grid, s);
+  else if (n <= 32) k2_launch_t<TB, CW, RS, Q4, 32>(p, grid, s);
+  else k2_launch_t<TB, CW, RS, Q4, kMaxLaunchSegs>(p, grid, s);
 }
 
-template <int CW, int RS>
+template <int CW, int RS, int Q4>
 static void k2_dispatch_tb(const K2Params& p, int grid, int tb, cudaStream_t s) {
   switch (tb) {
-    case 1: k2_launch_cap<1, CW, RS>(p, grid, s); break;
+    case 1: k2_launch_cap<1, CW, RS, Q4>(p, grid, s); break;
     case 2:
-      if constexpr (RS <= 8) k2_launch_cap<2, CW, RS>(p, grid, s);
+      if constexpr (RS <= 8) k2_launch_cap<2, CW, RS, Q4>(p, grid, s);
       break;
     default:
-      if constexpr (RS <= 4) k2_launch_cap<4, CW, RS>(p, grid, s);
+      if constexpr (RS <= 4) k2_launch_cap<4, CW, RS, Q4>(p, grid, s);
       break;
   }
 }
 
+// (CW, RS): bf16 d > 2048 -> (8, 2), d > 1024 -> (4, 4), d > 512 -> (4, 8), else (4, 16);
+// Q4G64 doubles RS up to 16: (8, 4), (4, 8), (4, 16), (4, 16)
 void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s) {
-  const int rs = k2_rows_per_tile(p.d);
-  if (k2_cw(p.d) == 8) k2_dispatch_tb<8, 2>(p, grid, tb, s);
-  else if (rs == 4) k2_dispatch_tb<4, 4>(p, grid, tb, s);
-  else if (rs == 8) k2_dispatch_tb<4, 8>(p, grid, tb, s);
-  else k2_dispatch_tb<4, 16>(p, grid, tb, s);
+  const int rs = k2_rows_per_tile(p.d, p.q4);
+  if (p.q4) {
+    if (k2_cw(p.d) == 8) k2_dispatch_tb<8, 4, 1>(p, grid, tb, s);
+    else if (rs == 8) k2_dispatch_tb<4, 8, 1>(p, grid, tb, s);
+    else k2_dispatch_tb<4, 16, 1>(p, grid, tb, s);
+    return;
+  }
+  if (k2_cw(p.d) == 8) k2_dispatch_tb<8, 2, 0>(p, grid, tb, s);
+  else if (rs == 4) k2_dispatch_tb<4, 4, 0>(p, grid, tb, s);
+  else if (rs == 8) k2_dispatch_tb<4, 8, 0>(p, grid, tb, s);
+  else k2_dispatch_tb<4, 16, 0>(p, grid, tb, s);
 }
 
-template <int TB, int CW, int RS>
+template <int TB, int CW, int RS, int Q4>
 static cudaError_t k2_attr() {
   cudaError_t e = cudaSuccess, r;
-  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, K2ParamsCap<8>>,
+  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, Q4, K2ParamsCap<8>>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) != cudaSuccess) e = r;
-  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, K2ParamsCap<32>>,
+  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, Q4, K2ParamsCap<32>>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) != cudaSuccess) e = r;
-  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, K2ParamsCap<kMaxLaunchSegs>>,
+  if ((r = cudaFuncSetAttribute(k2_split_expert<TB, CW, RS, Q4, K2ParamsCap<kMaxLaunchSegs>>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) != cudaSuccess) e = r;
   return e;
 }
@@ -449,12 +477,15 @@ static cudaError_t k2_attr() {
 bool kernels_init(char* err, size_t errlen) {
   cudaError_t e = cudaSuccess;
   cudaError_t r;
-#define MOEPIC_ATTR(TB, CW, RS) \
-  if ((r = k2_attr<TB, CW, RS>()) != cudaSuccess) e = r;
-  MOEPIC_ATTR(1, 8, 2) MOEPIC_ATTR(2, 8, 2) MOEPIC_ATTR(4, 8, 2)
-  MOEPIC_ATTR(1, 4, 4) MOEPIC_ATTR(2, 4, 4) MOEPIC_ATTR(4, 4, 4)
-  MOEPIC_ATTR(1, 4, 8) MOEPIC_ATTR(2, 4, 8)
-  MOEPIC_ATTR(1, 4, 16)
+#define MOEPIC_ATTR(TB, CW, RS, Q4) \
+  if ((r = k2_attr<TB, CW, RS, Q4>()) != cudaSuccess) e = r;
+  MOEPIC_ATTR(1, 8, 2, 0) MOEPIC_ATTR(2, 8, 2, 0) MOEPIC_ATTR(4, 8, 2, 0)
+  MOEPIC_ATTR(1, 4, 4, 0) MOEPIC_ATTR(2, 4, 4, 0) MOEPIC_ATTR(4, 4, 4, 0)
+  MOEPIC_ATTR(1, 4, 8, 0) MOEPIC_ATTR(2, 4, 8, 0)
+  MOEPIC_ATTR(1, 4, 16, 0)
+  MOEPIC_ATTR(1, 8, 4, 1) MOEPIC_ATTR(2, 8, 4, 1) MOEPIC_ATTR(4, 8, 4, 1)
+  MOEPIC_ATTR(1, 4, 8, 1) MOEPIC_ATTR(2, 4, 8, 1)
+  MOEPIC_ATTR(1, 4, 16, 1)
 #undef MOEPIC_ATTR
   if ((r = router_init()) != cudaSuccess) e = r;
   if ((r = combine_init()) != cudaSuccess) e = r;

@@ -76,6 +76,7 @@ struct K2Params {
   float* ws;              // partial sums
   int64_t total_rows;
   int d, K, nsegs;
+  int q4;                 // rows are Q4G64 (dequantised on the fly) instead of bf16
   Seg segs[kMaxLaunchSegs];
   // fused combine (the step's final K2 launch, cooperative): after a grid barrier every CTA adds
   // a slice of the step's partials in K3's fixed order
@@ -89,9 +90,9 @@ struct K2Params {
 };
 // Partition rule shared with the host: CTA c of G owns launch rows [c*R/G, (c+1)*R/G).
 MOEPIC_HD inline int64_t k2_row_lo(int64_t c, int64_t R, int64_t G) { return c * R / G; }
-int k2_rows_per_tile(int d);
-int k2_max_tokens(int d);
-size_t k2_smem_bytes(int d);
+int k2_rows_per_tile(int d, int q4);
+int k2_max_tokens(int d, int q4);
+size_t k2_smem_bytes(int d, int q4);
 void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s);
 
 // ------------------------------------------------------------------ K3: combine

@@ -68,7 +68,17 @@ std::string validate_desc(const moepic_model_desc* d) {
   if (d->tp_size < 1 || d->tp_rank < 0 || d->tp_rank >= d->tp_size) return "tp_rank / tp_size invalid";
   if (d->tp_size > 1 && d->ep_size != 1) return "tp_size > 1 needs ep_size == 1";
   if (d->I % ((int64_t)d->tp_size * d->row_granule) != 0) return "I must be a multiple of tp_size * row_granule";
+  if (d->weight_format != MOEPIC_BF16 && d->weight_format != MOEPIC_Q4G64) return "weight_format invalid";
+  if (d->weight_format == MOEPIC_Q4G64 && (d->d % 64 != 0 || d->max_batch > kDecodeMaxB))
+    return "Q4G64 experts need d % 64 == 0 and max_batch <= 32";
   return "";
+}
+
+// Bytes of one interleaved expert row in the stored format: bf16 [gate|up|down]
+// = 6d; Q4G64 = 3 x d/2 code bytes + 3 x d/64 (scale, min) bf16 pairs, padded to 16.
+uint64_t row_bytes_of(const moepic_model_desc& d) {
+  if (d.weight_format == MOEPIC_Q4G64) return (3ull * (d.d / 2) + 3ull * (d.d / 64) * 4 + 15) / 16 * 16;
+  return 6ull * d.d;
 }
 
 // The context works on its tensor-parallel slice: I/tp_size rows of every expert (SURVEY
@@ -86,7 +96,7 @@ inline bool adds_residual(const moepic_model_desc& d, uint32_t flags) {
 
 ArenaLayout arena_layout(const moepic_model_desc& d) {
   ArenaLayout a{};
-  const uint64_t rb = 6ull * d.d;
+  const uint64_t rb = row_bytes_of(d);
   const int Nl = n_local(d);
   size_t off = 0;
   a.routers = off; off = align_up(off + (size_t)d.L * d.N * d.d * 2);
@@ -349,7 +359,7 @@ struct moepic_ctx {
   uint8_t* scratch_d = nullptr;      // its device alias
   size_t scratch_bytes = 0;
 
-  uint64_t rb() const { return 6ull * desc.d; }
+  uint64_t rb() const { return row_bytes_of(desc); }
   int Nl() const { return n_local(desc); }
   int first_local() const { return desc.ep_rank * Nl(); }
   const uint8_t* host_expert(int layer, int e) const {
@@ -414,6 +424,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   ctx->arena = static_cast<uint8_t*>(dev_arena);
   ctx->cp.reset(new ControlPlane(desc->L, desc->N, desc->K, desc->d, desc->I, desc->row_granule,
                                  desc->buffer_experts, desc->n_shared, desc->ep_rank, desc->ep_size));
+  ctx->cp->row_bytes = (int64_t)row_bytes_of(*desc);
   char kerr[256];
   auto bail = [&](moepic_status st) {
     moepic_destroy(ctx);
@@ -466,8 +477,8 @@ moepic_status moepic_load_router(moepic_ctx* ctx, int32_t layer, const uint16_t*
 
 // HF layout -> row-interleaved rows [gate_r | up_r | down[:, r]] for r in [r0, r0 + I); the HF
 // tensors hold I_full rows (gate/up [I_full][d], down [d][I_full]); r0 = tp_rank * I.
-static void pack_rows(uint8_t* dst, const uint16_t* gate, const uint16_t* up, const uint16_t* down, int d,
-                      int I, int r0, int I_full) {
+static void pack_rows_bf16(uint8_t* dst, const uint16_t* gate, const uint16_t* up, const uint16_t* down, int d,
+                           int I, int r0, int I_full) {
   gate += (size_t)r0 * d;
   up += (size_t)r0 * d;
   down += r0;
@@ -490,6 +501,81 @@ static void pack_rows(uint8_t* dst, const uint16_t* gate, const uint16_t* up, co
   }
 }
 
+static inline float bf16f(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+static inline uint16_t bf16_down(float v) {   // largest bf16 <= v (finite v)
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  uint16_t t = (uint16_t)(u >> 16);
+  if (v < 0 && bf16f(t) > v) ++t;
+  return t;
+}
+static inline uint16_t bf16_up(float v) {     // smallest bf16 >= v (v >= 0)
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  uint16_t t = (uint16_t)(u >> 16);
+  if (bf16f(t) < v) ++t;
+  return t;
+}
+
+// Q4G64 (reading Q28): per stored row vector and group of 64 entries, lo_b = bf16 round
+// down of the minimum, s_b = bf16 round up of fp32((max - lo_b) / 15) (1.0 if 0), code =
+// clamp(rint(fp32(fp32(x - lo_b) / s_b)), 0, 15) — fp32, this order, no contraction (the file is
+// compiled with -ffp-contract=off), so codes equal the oracle's bit for bit.
+static void quantize_group(const float* x, uint8_t* codes /*32 bytes*/, uint32_t* param) {
+  float lo = x[0], hi = x[0];
+  for (int k = 1; k < 64; ++k) {
+    lo = std::min(lo, x[k]);
+    hi = std::max(hi, x[k]);
+  }
+  const uint16_t lob = bf16_down(lo);
+  const float lof = bf16f(lob);
+  const float t = (hi - lof) / 15.0f;
+  uint16_t sb = bf16_up(t);
+  if (sb == 0) sb = 0x3F80;
+  const float sf = bf16f(sb);
+  for (int k = 0; k < 64; k += 2) {
+    float q0 = std::nearbyint((x[k] - lof) / sf), q1 = std::nearbyint((x[k + 1] - lof) / sf);
+    q0 = std::min(15.0f, std::max(0.0f, q0));
+    q1 = std::min(15.0f, std::max(0.0f, q1));
+    codes[k / 2] = (uint8_t)((int)q0 | ((int)q1 << 4));
+  }
+  *param = (uint32_t)sb | ((uint32_t)lob << 16);
+}
+
+static void pack_rows_q4(uint8_t* dst, const uint16_t* gate, const uint16_t* up, const uint16_t* down, int d, int I,
+                         int r0, int I_full, uint64_t rb) {
+  const int ng = d / 64;
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < I; ++r) {
+    uint8_t* row = dst + (uint64_t)r * rb;
+    memset(row, 0, rb);
+    std::vector<float> x(d);
+    for (int part = 0; part < 3; ++part) {
+      for (int k = 0; k < d; ++k)
+        x[k] = bf16f(part == 0 ? gate[(size_t)(r0 + r) * d + k]
+                     : part == 1 ? up[(size_t)(r0 + r) * d + k] : down[(size_t)k * I_full + r0 + r]);
+      for (int g = 0; g < ng; ++g) {
+        uint32_t prm;
+        quantize_group(&x[(size_t)g * 64], row + (size_t)part * (d / 2) + (size_t)g * 32, &prm);
+        memcpy(row + 3ull * (d / 2) + ((size_t)part * ng + g) * 4, &prm, 4);
+      }
+    }
+  }
+}
+
+static void pack_rows(const moepic_model_desc& d, uint8_t* dst, const uint16_t* gate, const uint16_t* up,
+                      const uint16_t* down, int I_full) {
+  if (d.weight_format == MOEPIC_Q4G64)
+    pack_rows_q4(dst, gate, up, down, d.d, d.I, d.tp_rank * d.I, I_full, row_bytes_of(d));
+  else
+    pack_rows_bf16(dst, gate, up, down, d.d, d.I, d.tp_rank * d.I, I_full);
+}
+
 moepic_status moepic_load_expert(moepic_ctx* ctx, int32_t layer, int32_t expert, const uint16_t* gate,
                                  const uint16_t* up, const uint16_t* down) {
   CTX_GUARD();
@@ -499,16 +585,30 @@ moepic_status moepic_load_expert(moepic_ctx* ctx, int32_t layer, int32_t expert,
     if (expert >= d.N) return fail(&ctx->err, MOEPIC_EINVAL, "expert out of range");
     if (layer < 0 || layer >= d.L_host) return fail(&ctx->err, MOEPIC_EINVAL, "layer must be < L_host");
     if (!ctx->cp->is_local(expert)) return MOEPIC_OK;   // another EP rank owns it
-    pack_rows(const_cast<uint8_t*>(ctx->host_expert(layer, expert)), gate, up, down, d.d, d.I,
-              d.tp_rank * d.I, ctx->I_full);
+    pack_rows(d, const_cast<uint8_t*>(ctx->host_expert(layer, expert)), gate, up, down, ctx->I_full);
     return MOEPIC_OK;
   }
   const int s = -1 - expert;
   if (s >= d.n_shared) return fail(&ctx->err, MOEPIC_EINVAL, "shared expert index out of range");
   if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
   std::vector<uint8_t> tmp((size_t)d.I * ctx->rb());
-  pack_rows(tmp.data(), gate, up, down, d.d, d.I, d.tp_rank * d.I, ctx->I_full);
+  pack_rows(d, tmp.data(), gate, up, down, ctx->I_full);
   CK(cudaMemcpy(ctx->shared_ptr(layer, s), tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_pack_expert(const moepic_model_desc* desc, const uint16_t* gate, const uint16_t* up,
+                                 const uint16_t* down, void* out, size_t* bytes) {
+  if (!bytes || !validate_desc(desc).empty()) return MOEPIC_EINVAL;
+  const moepic_model_desc l = local_desc(*desc);
+  const size_t need = (size_t)l.I * row_bytes_of(l);
+  if (!out) {
+    *bytes = need;
+    return MOEPIC_OK;
+  }
+  if (*bytes < need || !gate || !up || !down) return MOEPIC_EINVAL;
+  pack_rows(l, static_cast<uint8_t*>(out), gate, up, down, desc->I);
+  *bytes = need;
   return MOEPIC_OK;
 }
 
@@ -566,7 +666,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
                                   cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb, int& launches,
                                   FuseCombine* fuse = nullptr) {
   const int d = ctx->desc.d;
-  const int tbmax = k2_max_tokens(d);
+  const int tbmax = k2_max_tokens(d, ctx->desc.weight_format == MOEPIC_Q4G64);
   // split by token groups of <= tbmax tokens
   std::vector<StepSeg> work;
   for (const auto& sg : segs) {
@@ -601,6 +701,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
     kp.ws = reinterpret_cast<float*>(ctx->arena + ctx->lay.ws);
     kp.total_rows = R;
     kp.d = d;
+    kp.q4 = ctx->desc.weight_format == MOEPIC_Q4G64;
     kp.K = ctx->desc.K;
     kp.nsegs = (int)(i1 - i0);
     int64_t rb = 0;
@@ -1420,6 +1521,7 @@ moepic_status moepic_hostsim_create(const moepic_model_desc* desc, moepic_hostsi
   hs->lay = arena_layout(*desc);
   hs->cp.reset(new ControlPlane(desc->L, desc->N, desc->K, desc->d, desc->I, desc->row_granule,
                                 desc->buffer_experts, desc->n_shared, desc->ep_rank, desc->ep_size));
+  hs->cp->row_bytes = (int64_t)row_bytes_of(*desc);
   *out = hs;
   return MOEPIC_OK;
 }
