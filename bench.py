@@ -132,7 +132,7 @@ def pcie_probe(torch, nbytes=1 << 30, reps=10):
     return best
 
 
-def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print, parallel="ep"):
+def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print, parallel="ep", weights="bf16"):
     """EP: rank owns experts [rank N/G, (rank+1) N/G).  TP (along I): rank owns rows
     [rank I/G, (rank+1) I/G) of every expert; budgets are then in units of that slice."""
     S = synth.SHAPES[cfg["shape"]]
@@ -145,7 +145,8 @@ def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print,
     desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=g,
                           max_batch=max_batch, renorm_topk=S.renorm, L_host=Lh, v_e_max=v_e,
                           ep_rank=0 if tp else rank, ep_size=1 if tp else world,
-                          tp_rank=rank if tp else 0, tp_size=world if tp else 1)
+                          tp_rank=rank if tp else 0, tp_size=world if tp else 1,
+                          weight_format=api.M.Q4G64 if weights == "q4" else api.M.BF16)
     t0 = time.time()
     ctx = api.MoEpic(desc)
     for i in range(L):
@@ -190,7 +191,7 @@ def run_ours(args, log):
     if world == 1:
         parallel = "single"
     ctx, desc, S, v_e, keep = build_model(api, synth, torch, cfg, rank, world, max_batch=cfg["B"], log=log,
-                                          parallel=parallel)
+                                          parallel=parallel, weights=args.weights)
     L, B = cfg["L"], cfg["B"]
     t0 = time.time()
     base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[S.K * B] * L, seed=0)
@@ -266,7 +267,8 @@ def run_ours(args, log):
         torch.cuda.synchronize()
         k2w = ctx.profile_read(api.M.KERNEL_EXPERT)
         ctx.profile(False)
-        U_e = 6 * S.d * (S.I // world if parallel == "tp" else S.I)   # bytes of one (local) expert
+        rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
+        U_e = rbytes * (S.I // world if parallel == "tp" else S.I)   # bytes of one (local) expert
         t_load = U_e / (pcie * 1e9) * 1e3                          # ms per full expert
         t_moe = k2w["total_ms"] / (adapt_tokens * L)               # ms of expert compute per layer-step
         t0 = time.time()
@@ -389,7 +391,8 @@ def run_ours(args, log):
         "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (seeded random weights, organic routing process; synth/)",
+        "dtype": "bf16" if args.weights == "bf16" else "q4g64 weights, f32 accumulate",
+        "data": "synthetic (seeded random weights, organic routing process; synth/)",
         "config": {"workload": _workload(cfg),
                    "model": f"{args.config}-shaped MoE layers (random init)", "layers": L, "L_host": cfg["L_host"],
                    "global_batch": B, "seq_len": 1,
@@ -398,6 +401,7 @@ def run_ours(args, log):
                        "all_gather(h) + reduce_scatter(y), T/G tokens per rank" if prefill and parallel == "ep"
                        else "all_reduce(y) of the per-rank partial outputs"),
                    "v_e_experts": base_cfg["v_e"], "theta": base_cfg["theta_i"][0], "mode": args.mode,
+                   "weights": args.weights,
                    "policy": MODES[args.mode].get("policy", "LCP"), "prefetch": base_cfg.get("prefetch", True),
                    "y_cap": S.K * B,
                    "alg1": None if solved is None else {"tau_tokens": args.tau, "theta_eff_min": min(solved["theta_eff_i"]),
@@ -552,6 +556,9 @@ def main():
     ap.add_argument("--mode", default="moepic", choices=sorted(MODES), help="ablation mode (SURVEY §8(f) NEXT-1)")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="time the step without the per-kernel CUDA events (roofline fields then empty)")
+    ap.add_argument("--weights", default="bf16", choices=["bf16", "q4"],
+                    help="expert storage: bf16 (default, the headline) or q4 = Q4G64 low-bit experts "
+                         "(SURVEY §8(f) NEXT-3; a reduced-precision mode, never the headline)")
     ap.add_argument("--parallel", default="auto", choices=["auto", "ep", "tp"],
                     help="N>1 sharding: tp = every expert split along I over the ranks (decode default), "
                          "ep = experts partitioned over the ranks (prefill default)")
