@@ -187,12 +187,12 @@ def moe_layer_tp_partial(h_bits, router_bits, experts, K, tp_rank, tp_size, shar
         ids = topk_ids(logits[b], K)
         w = gate_weights(logits[b], ids, renorm)
         for k, e in enumerate(ids):
-            g, u, dn = (bf16_to_f64(x) for x in get(int(e)))
+            g, u, dn = (weights_f64(x) for x in get(int(e)))
             I = g.shape[0]
             lo, hi = tp_rank * I // tp_size, (tp_rank + 1) * I // tp_size
             y[b] += w[k] * expert_forward(h[b:b + 1], g[lo:hi], u[lo:hi], dn[:, lo:hi])[0]
     for (gate, up, down) in shared:
-        g, u, dn = bf16_to_f64(gate), bf16_to_f64(up), bf16_to_f64(down)
+        g, u, dn = weights_f64(gate), weights_f64(up), weights_f64(down)
         I = g.shape[0]
         lo, hi = tp_rank * I // tp_size, (tp_rank + 1) * I // tp_size
         y += expert_forward(h, g[lo:hi], u[lo:hi], dn[:, lo:hi])

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, B):
+def _worker(rank, world, port, q, B, fmt=0):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -38,8 +38,14 @@ def _worker(rank, world, port, q, B):
         from paper_2509_08342_b200 import api
         L, N, K, d, I = 2, 8, 2, 256, 512
         m = Model(L, N, K, d, I, n_shared=1, seed=23)
+        expert, shared_of = m.expert, (lambda i, s: m.shared[(i, s)])
+        if fmt:   # Q4G64: the oracle sees the dequantised experts (slicing rows commutes with it)
+            from oracle import quant as Qz
+            deq = {k: Qz.dequantize_expert(Qz.quantize_expert(*w)) for k, w in m.experts.items()}
+            dsh = {k: Qz.dequantize_expert(Qz.quantize_expert(*w)) for k, w in m.shared.items()}
+            expert, shared_of = (lambda i, e: deq[(i % m.L_host, e)]), (lambda i, s: dsh[(i, s)])
         desc = api.model_desc(L, N, K, d, I, n_shared=1, row_granule=64, max_batch=B, v_e_max=8.0,
-                              tp_rank=rank, tp_size=world)
+                              tp_rank=rank, tp_size=world, weight_format=fmt)
         ctx = api.MoEpic(desc)
         m.load_into(ctx)
         cfg = ctx.configure(v_e=3.0, theta_i=[0.5, 0.5], seed=1)
@@ -58,14 +64,14 @@ def _worker(rank, world, port, q, B):
                 g = [torch.zeros_like(sig) for _ in range(world)]
                 dist.all_gather(g, sig)
                 assert all(torch.equal(g[0], v) for v in g), "ranks took different decisions"
-                shared = [m.shared[(i, s)] for s in range(m.n_shared)]
-                part = ON.moe_layer_tp_partial(hb, m.routers[i], lambda e: m.expert(i, e), K, rank, world,
+                shared = [shared_of(i, s) for s in range(m.n_shared)]
+                part = ON.moe_layer_tp_partial(hb, m.routers[i], lambda e: expert(i, e), K, rank, world,
                                                shared=shared)
                 hres = ON.bf16_to_f64(hb) if (t == 1 and rank == 0) else 0.0
                 yc = y.cpu()
                 worst_part = max(worst_part, rel_err(yc.numpy(), part + hres))
                 dist.all_reduce(yc)                          # the TP combine
-                y_ref, _, _, _ = m.oracle_layer(i, hb)
+                y_ref, _, _, _ = ON.moe_layer(hb, m.routers[i], lambda e: expert(i, e), K, shared=shared)
                 if t == 1:
                     y_ref = y_ref + ON.bf16_to_f64(hb)
                 worst_sum = max(worst_sum, rel_err(yc.numpy(), y_ref))
@@ -81,14 +87,14 @@ def _worker(rank, world, port, q, B):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B", [1, 5, 64])
-def test_tp_two_ranks_one_gpu(B):
+@pytest.mark.parametrize("B,fmt", [(1, 0), (5, 0), (64, 0), (1, 1), (5, 1)])
+def test_tp_two_ranks_one_gpu(B, fmt):
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, B)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, B, fmt)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=600) for _ in ps)
