@@ -325,7 +325,12 @@ std::string ControlPlane::configure(const CacheParams& p, uint64_t slot_pool_row
 }
 
 void ControlPlane::step(int layer, const int32_t* ids, int B, const Plan* plan, StepResult& out) {
-  LayerState& l = layers[layer];
+  classify(layer, ids, B, plan, out);
+  commit(layer, ids, B, plan, out);
+}
+
+void ControlPlane::classify(int layer, const int32_t* ids, int B, const Plan* plan, StepResult& out) {
+  const LayerState& l = layers[layer];
   out = StepResult();
   // 1. activation set (local experts), order (B_e desc, id asc)
   std::vector<int32_t> be(N, 0);
@@ -337,14 +342,10 @@ void ControlPlane::step(int layer, const int32_t* ids, int B, const Plan* plan, 
     if (be[a] != be[b]) return be[a] > be[b];
     return a < b;
   });
-  // 2. statistics on pre-step counts, prediction = the ranking that planned this layer
-  l.st.observe(ids, B, K, plan ? plan->ranking.data() : nullptr);
   // 3. classification against the state before the step
   std::vector<int32_t> pidx(N, -1);
   if (plan)
     for (size_t j = 0; j < plan->items.size(); ++j) pidx[plan->items[j].expert] = (int32_t)j;
-  std::vector<char> inA(N, 0);
-  for (int e : out.A) inA[e] = 1;
   for (int e : out.A) {
     bool cached = l.cached(e);
     int pj = pidx[e];
@@ -360,6 +361,18 @@ void ControlPlane::step(int layer, const int32_t* ids, int B, const Plan* plan, 
     if (c == kAlpha) ++out.alpha; else if (c == kBeta) ++out.beta; else ++out.gamma;
     if (pj >= 0) ++out.pred_hits;
   }
+}
+
+void ControlPlane::commit(int layer, const int32_t* ids, int B, const Plan* plan, StepResult& out) {
+  LayerState& l = layers[layer];
+  // 2. statistics on pre-step counts, prediction = the ranking that planned this layer
+  l.st.observe(ids, B, K, plan ? plan->ranking.data() : nullptr);
+  std::vector<char> inA(N, 0);
+  std::vector<int32_t> be(N, 0);
+  for (size_t a = 0; a < out.A.size(); ++a) {
+    inA[out.A[a]] = 1;
+    be[out.A[a]] = out.Be[a];
+  }
   // 4. counters: update first, then choose victims (Q12)
   const int64_t s = l.step_no;
   for (int e = 0; e < N; ++e) {
@@ -367,7 +380,10 @@ void ControlPlane::step(int layer, const int32_t* ids, int B, const Plan* plan, 
     else l.nu[e] += 1;
   }
   l.step_no = s + 1;
-  // 5. admission in A order (Q11; victims exclude A)
+  // 5. admission in A order (Q11; victims exclude A).  The keys depend only on
+  // (mu, nu, last), fixed once the counters are updated, so each candidate's key is computed once
+  // per step however many admissions look at it.
+  std::vector<double> key;
   if (l.cache_on()) {
     for (size_t a = 0; a < out.A.size(); ++a) {
       int e = out.A[a];
@@ -391,11 +407,16 @@ void ControlPlane::step(int layer, const int32_t* ids, int B, const Plan* plan, 
           uint64_t z = splitmix64_next(l.rnd);
           v = cands[(size_t)(z % (uint64_t)cands.size())];
         } else {
+          if (key.empty()) {
+            key.assign(N, 0.0);
+            for (int x = 0; x < N; ++x)
+              if (l.slot_of[x] >= 0 && !inA[x]) key[x] = policy_key(cfg.policy, l, x, cfg.rho, cfg.omega);
+          }
           v = cands[0];
-          double kv = policy_key(cfg.policy, l, v, cfg.rho, cfg.omega);
+          double kv = key[v];
           for (size_t j = 1; j < cands.size(); ++j) {
             int x = cands[j];
-            double kx = policy_key(cfg.policy, l, x, cfg.rho, cfg.omega);
+            double kx = key[x];
             if (kx < kv || (kx == kv && l.nu[x] > l.nu[v])) { v = x; kv = kx; }
             // equal key and nu: keep the smaller id (cands ascending)
           }

@@ -136,8 +136,13 @@ class ControlPlane {
   std::string configure(const CacheParams& p, uint64_t slot_pool_rows);
 
   // One layer step (state before the call is what classification sees).  `plan` is the plan
-  // made for this layer (or null).  ids: [B][K].
+  // made for this layer (or null).  ids: [B][K].  step = classify + commit; the library issues
+  // the copies that classification alone decides (beta bottoms) between the two.
   void step(int layer, const int32_t* ids, int B, const Plan* plan, StepResult& out);
+  // activation set A (B_e desc, id asc) and classes against the state before the step
+  void classify(int layer, const int32_t* ids, int B, const Plan* plan, StepResult& out);
+  // statistics, counters, admissions and on-demand bytes of a classified step
+  void commit(int layer, const int32_t* ids, int B, const Plan* plan, StepResult& out);
 
   // Build the prefetch plan for layer j from ranking R'.
   void make_plan(int j, const int32_t* ranking, Plan& out) const;

@@ -297,6 +297,12 @@ struct moepic_ctx {
     feed_cancel.clear();
   }
 
+  bool host_timing = getenv("MOEPIC_HOST_TIMING") != nullptr;
+  double ht[4] = {0, 0, 0, 0};
+  double hc[2] = {0, 0};
+  double hp[4] = {0, 0, 0, 0};
+  uint64_t hc_n = 0;
+  uint64_t ht_n = 0;
   unsigned long long* k1dbg = nullptr;   // MOEPIC_K1_TRACE ring (tools)
   uint64_t k1dbg_n = 0;
   bool profiling = false;
@@ -937,7 +943,7 @@ static moepic_status finish_plan(moepic_ctx* ctx, const Plan& plan, const StepRe
     return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch copy: %s", cudaGetErrorString(cudaGetLastError()));
   }
   ctx->feed_drop();
-  CK(cudaEventRecord(ctx->ev_plan[plan.buf], ctx->copy));
+  if (!plan.items.empty()) CK(cudaEventRecord(ctx->ev_plan[plan.buf], ctx->copy));   // gB waits on it
   return MOEPIC_OK;
 }
 
@@ -1138,17 +1144,26 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   const int buf = have_plan ? used.buf : (ctx->last_buf ^ 1);
 
   // ---- K1 (router + fused next-layer predictor) and the mailbox handoff
+  const auto t_call = std::chrono::steady_clock::now();
   moepic_status st = run_router(ctx, h, B, layer, predict ? j : -1, s, true, false);
+  const auto t_routed = std::chrono::steady_clock::now();
+  auto t_first_copy = t_routed;   // MOEPIC_HOST_TIMING
   if (st != MOEPIC_OK) return st;
   ++launches;
 
   // ---- control plane (classification, counters, admission)
+  // ---- control plane: classification first; the beta bottoms it decides are issued on
+  // the copy stream before the rest of the step (statistics, counters, admissions) is computed,
+  // so the link starts streaming this layer's missing rows as early as possible
   StepResult res;
-  cp.step(layer, ctx->ids_h.data(), B, have_plan ? &used : nullptr, res);
+  const Plan* up = have_plan ? &used : nullptr;
+  cp.classify(layer, ctx->ids_h.data(), B, up, res);
+  const auto t_cls = std::chrono::steady_clock::now();
   if (have_plan) {
     st = finish_plan(ctx, used, res);
     if (st != MOEPIC_OK) return st;
   }
+  const auto t_fin = std::chrono::steady_clock::now();
 
   // token masks per activated expert
   const int K = d.K;
@@ -1160,81 +1175,98 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
         if (ctx->ids_h[b * K + k] == e) m |= 1u << b;
     return m;
   };
-  std::vector<int32_t> adm_slot(d.N, -2);   // expert -> slot for admitted, -1 if not admitted
-  for (const auto& a : res.adm) adm_slot[a.expert] = a.victim == kAdmNone ? -1 : a.slot;
 
-  // ---- segment groups: resident now (A), prefetched (B, plan event), on-demand (C, copy event).
-  // The on-demand copies are issued before the first K2 launch: the link is the bottleneck, so it
-  // starts streaming as early as possible (issuing the resident launch first shortened the K2
-  // launches' event time by ~5 us but cost ~1% of decode throughput on the B200).
-  struct Copy { uint8_t* dst; const uint8_t* src; size_t bytes; };
-  std::vector<Copy> copies;
+  // ---- segment groups: resident now (A), prefetched (B, plan event), on-demand (C, copy event)
   std::vector<StepSeg> gA, gB, gC;
   int64_t od_row = 0;
+  int n_od = 0;
+  bool waited = false;
+  auto copy = [&](uint8_t* dst, const uint8_t* src, size_t bytes) -> moepic_status {
+    const auto tw0 = std::chrono::steady_clock::now();
+    if (!waited) {   // the buffers / slots written here were last read by earlier steps
+      for (int b2 = 0; b2 < 2; ++b2)
+        if (ctx->ev_step_rec[b2]) CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[b2], 0));
+      waited = true;
+    }
+    const auto tw1 = std::chrono::steady_clock::now();
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
+    if (ctx->host_timing) {
+      ctx->hc[0] += std::chrono::duration<double, std::micro>(tw1 - tw0).count();
+      ctx->hc[1] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw1).count();
+      ctx->hc_n++;
+    }
+    ctx->ctr.h2d_copies++;
+    if (n_od++ == 0 && ctx->host_timing) t_first_copy = std::chrono::steady_clock::now();
+    return MOEPIC_OK;
+  };
   const uint32_t all_tok = B >= 32 ? 0xFFFFFFFFu : ((1u << B) - 1u);
   {
     const int64_t lo = shared_lo(cp), hi = shared_hi(cp);
     for (int s2 = 0; s2 < d.n_shared; ++s2)
       if (hi > lo) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2) + lo * rb, -1 - s2, (int32_t)(hi - lo), all_tok, (int32_t)lo});
   }
-  for (size_t a = 0; a < res.A.size(); ++a) {
+  std::vector<uint32_t> masks(res.A.size());
+  for (size_t a = 0; a < res.A.size(); ++a) {   // pass 1: everything classification decides
     const int e = res.A[a];
-    const uint32_t m = mask_of(e);
+    const uint32_t m = masks[a] = mask_of(e);
     const int c = res.cls[a];
     const int pj = res.plan_idx[a];
-    const uint8_t* hsrc = ctx->host_expert(layer, e);
     const bool top_cached_before = (c != kGamma) && !(pj >= 0 && used.items[pj].full);
-    if (top_cached_before && l.I_top > 0) {
-      gA.push_back(StepSeg{ctx->slot_ptr(layer, l.slot_of[e]), e, l.I_top, m, 0});
-    }
+    if (top_cached_before && l.I_top > 0) gA.push_back(StepSeg{ctx->slot_ptr(layer, l.slot_of[e]), e, l.I_top, m, 0});
     if (pj >= 0) {
       const PlanItem& it = used.items[pj];
       gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m, it.full ? 0 : l.I_top});
-      continue;   // alpha: nothing missing
-    }
-    if (c == kBeta) {
+    } else if (c == kBeta) {
       const int rows = d.I - l.I_top;
       uint8_t* dst = ctx->od_ptr(buf, od_row);
-      copies.push_back({dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows * rb});
+      if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+      if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)l.I_top * rb, (size_t)rows * rb)) != MOEPIC_OK) return st;
       gC.push_back(StepSeg{dst, e, rows, m, l.I_top});
       od_row += rows;
-    } else if (c == kGamma) {
-      const int slot = adm_slot[e];
-      if (slot >= 0 && l.I_top > 0) {
-        uint8_t* top = ctx->slot_ptr(layer, slot);
-        copies.push_back({top, hsrc, (size_t)l.I_top * rb});
-        gC.push_back(StepSeg{top, e, l.I_top, m, 0});
-        const int rows = d.I - l.I_top;
-        if (rows > 0) {
-          uint8_t* dst = ctx->od_ptr(buf, od_row);
-          copies.push_back({dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows * rb});
-          gC.push_back(StepSeg{dst, e, rows, m, l.I_top});
-          od_row += rows;
-        }
-      } else {
-        uint8_t* dst = ctx->od_ptr(buf, od_row);
-        copies.push_back({dst, hsrc, (size_t)d.I * rb});
-        gC.push_back(StepSeg{dst, e, d.I, m, 0});
-        od_row += d.I;
-      }
     }
   }
-  if ((uint64_t)od_row > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
-  // on-demand copies (transfer engine, copy stream, FIFO after the pending prefetch)
-  auto issue_copies = [&]() -> moepic_status {
-    for (int b2 = 0; b2 < 2; ++b2)
-      if (ctx->ev_step_rec[b2]) CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[b2], 0));
-    for (const Copy& c : copies) {
-      CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, ctx->copy));
-      ctx->ctr.h2d_copies++;
+  const auto t_p1 = std::chrono::steady_clock::now();
+  cp.commit(layer, ctx->ids_h.data(), B, up, res);
+  const auto t_com = std::chrono::steady_clock::now();
+  if (ctx->host_timing) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    ctx->hp[0] += us(t_routed, t_cls);
+    ctx->hp[1] += us(t_cls, t_fin);
+    ctx->hp[2] += us(t_fin, t_p1);
+    ctx->hp[3] += us(t_p1, t_com);
+  }
+  std::vector<int32_t> adm_slot(d.N, -2);   // expert -> slot for admitted, -1 if not admitted
+  for (const auto& a : res.adm) adm_slot[a.expert] = a.victim == kAdmNone ? -1 : a.slot;
+  for (size_t a = 0; a < res.A.size(); ++a) {   // pass 2: gamma experts (their top goes to the admitted slot)
+    if (res.cls[a] != kGamma || res.plan_idx[a] >= 0) continue;
+    const int e = res.A[a];
+    const uint32_t m = masks[a];
+    const uint8_t* hsrc = ctx->host_expert(layer, e);
+    const int slot = adm_slot[e];
+    const int rows_od = (slot >= 0 && l.I_top > 0) ? d.I - l.I_top : d.I;
+    if ((uint64_t)(od_row + rows_od) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+    if (slot >= 0 && l.I_top > 0) {
+      uint8_t* top = ctx->slot_ptr(layer, slot);
+      if ((st = copy(top, hsrc, (size_t)l.I_top * rb)) != MOEPIC_OK) return st;
+      gC.push_back(StepSeg{top, e, l.I_top, m, 0});
+      if (rows_od > 0) {
+        uint8_t* dst = ctx->od_ptr(buf, od_row);
+        if ((st = copy(dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows_od * rb)) != MOEPIC_OK) return st;
+        gC.push_back(StepSeg{dst, e, rows_od, m, l.I_top});
+        od_row += rows_od;
+      }
+    } else {
+      uint8_t* dst = ctx->od_ptr(buf, od_row);
+      if ((st = copy(dst, hsrc, (size_t)d.I * rb)) != MOEPIC_OK) return st;
+      gC.push_back(StepSeg{dst, e, d.I, m, 0});
+      od_row += d.I;
     }
-    if (!copies.empty()) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
-    return MOEPIC_OK;
-  };
+  }
+  if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
+  const auto t_copies = std::chrono::steady_clock::now();
 
   if (B > kDecodeMaxB) {
     // ---- prefill: permute, tcgen05 GEMMs per segment group, combine
-    if ((st = issue_copies()) != MOEPIC_OK) return st;
     st = prefill_launch(ctx, h, B, y_dev, s, flags, gA, gB, gC, buf, launches);
     if (st != MOEPIC_OK) return st;
   } else {
@@ -1243,7 +1275,6 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   std::vector<CombineSeg> comb;
   FuseCombine fuse{y_dev, adds_residual(d, flags) ? 1 : 0, false};
   const bool lastA = gB.empty() && gC.empty(), lastB = gC.empty();
-  if ((st = issue_copies()) != MOEPIC_OK) return st;
   st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches, lastA ? &fuse : nullptr);
   if (st != MOEPIC_OK) return st;
   if (!gB.empty()) {
@@ -1302,6 +1333,15 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     ctx->pending = next;
   }
 
+  if (ctx->host_timing) {   // MOEPIC_HOST_TIMING (tools): host-side phases of the call, us
+    const auto t_end = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    ctx->ht[0] += us(t_call, t_routed);
+    ctx->ht[1] += us(t_routed, n_od ? t_first_copy : t_copies);
+    ctx->ht[2] += us(t_routed, t_copies);
+    ctx->ht[3] += us(t_copies, t_end);
+    ctx->ht_n++;
+  }
   // ---- trace + counters
   const uint64_t pb = predict ? plan_bytes(next, (int64_t)rb) : 0;
   const uint64_t hbm = step_hbm_bytes(cp, res, B, predict ? 2 : 1, pb);
@@ -1466,6 +1506,16 @@ const char* moepic_last_error(const moepic_ctx* ctx) { return ctx ? ctx->err.c_s
 void moepic_destroy(moepic_ctx* ctx) {
   if (!ctx) return;
   cudaDeviceSynchronize();
+  if (ctx->ht_n)
+    fprintf(stderr, "[hosttiming] %llu calls: launch router + wait routing %.1f | routing -> first copy issued %.1f | "
+            "routing -> all copies issued %.1f | K2 launches + next plan %.1f us\n", (unsigned long long)ctx->ht_n,
+            ctx->ht[0] / ctx->ht_n, ctx->ht[1] / ctx->ht_n, ctx->ht[2] / ctx->ht_n, ctx->ht[3] / ctx->ht_n);
+  if (ctx->ht_n)
+    fprintf(stderr, "[hosttiming] classify %.1f, finish_plan %.1f, pass 1 %.1f, commit %.1f us\n", ctx->hp[0] / ctx->ht_n,
+            ctx->hp[1] / ctx->ht_n, ctx->hp[2] / ctx->ht_n, ctx->hp[3] / ctx->ht_n);
+  if (ctx->hc_n)
+    fprintf(stderr, "[hosttiming] %llu copies: stream waits %.1f us, cudaMemcpyAsync %.1f us per copy\n",
+            (unsigned long long)ctx->hc_n, ctx->hc[0] / ctx->hc_n, ctx->hc[1] / ctx->hc_n);
   if (ctx->k1dbg) {   // MOEPIC_K1_TRACE summary: mean phase offsets from the first CTA start (us)
     std::vector<unsigned long long> h(4096 * 8);
     cudaMemcpy(h.data(), ctx->k1dbg, h.size() * 8, cudaMemcpyDeviceToHost);
