@@ -1216,7 +1216,9 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     if (pj >= 0) {
       const PlanItem& it = used.items[pj];
       gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m, it.full ? 0 : l.I_top});
-    } else if (c == kBeta) {
+    } else if (c == kBeta || (c == kGamma && l.I_top < d.I)) {
+      // missing bottom rows [I_top, I): known from classification alone (a gamma expert's top
+      // rows follow in pass 2, once admission has chosen their destination)
       const int rows = d.I - l.I_top;
       uint8_t* dst = ctx->od_ptr(buf, od_row);
       if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
@@ -1237,32 +1239,30 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   }
   std::vector<int32_t> adm_slot(d.N, -2);   // expert -> slot for admitted, -1 if not admitted
   for (const auto& a : res.adm) adm_slot[a.expert] = a.victim == kAdmNone ? -1 : a.slot;
-  for (size_t a = 0; a < res.A.size(); ++a) {   // pass 2: gamma experts (their top goes to the admitted slot)
-    if (res.cls[a] != kGamma || res.plan_idx[a] >= 0) continue;
+  for (size_t a = 0; a < res.A.size(); ++a) {   // pass 2: gamma tops -> the admitted slot (or the od region)
+    if (res.cls[a] != kGamma || res.plan_idx[a] >= 0 || l.I_top == 0) continue;
     const int e = res.A[a];
-    const uint32_t m = masks[a];
-    const uint8_t* hsrc = ctx->host_expert(layer, e);
     const int slot = adm_slot[e];
-    const int rows_od = (slot >= 0 && l.I_top > 0) ? d.I - l.I_top : d.I;
-    if ((uint64_t)(od_row + rows_od) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
-    if (slot >= 0 && l.I_top > 0) {
-      uint8_t* top = ctx->slot_ptr(layer, slot);
-      if ((st = copy(top, hsrc, (size_t)l.I_top * rb)) != MOEPIC_OK) return st;
-      gC.push_back(StepSeg{top, e, l.I_top, m, 0});
-      if (rows_od > 0) {
-        uint8_t* dst = ctx->od_ptr(buf, od_row);
-        if ((st = copy(dst, hsrc + (uint64_t)l.I_top * rb, (size_t)rows_od * rb)) != MOEPIC_OK) return st;
-        gC.push_back(StepSeg{dst, e, rows_od, m, l.I_top});
-        od_row += rows_od;
-      }
+    uint8_t* top;
+    if (slot >= 0) {
+      top = ctx->slot_ptr(layer, slot);
     } else {
-      uint8_t* dst = ctx->od_ptr(buf, od_row);
-      if ((st = copy(dst, hsrc, (size_t)d.I * rb)) != MOEPIC_OK) return st;
-      gC.push_back(StepSeg{dst, e, d.I, m, 0});
-      od_row += d.I;
+      if ((uint64_t)(od_row + l.I_top) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+      top = ctx->od_ptr(buf, od_row);
+      od_row += l.I_top;
     }
+    if ((st = copy(top, ctx->host_expert(layer, e), (size_t)l.I_top * rb)) != MOEPIC_OK) return st;
+    gC.push_back(StepSeg{top, e, l.I_top, masks[a], 0});
   }
   if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
+  {   // an expert's on-demand segments consecutive, tops first (the prefill down GEMM groups by expert)
+    std::vector<int32_t> pos(d.N, 0);
+    for (size_t a = 0; a < res.A.size(); ++a) pos[res.A[a]] = (int32_t)a;
+    std::stable_sort(gC.begin(), gC.end(), [&](const StepSeg& x, const StepSeg& y) {
+      const int px = x.expert >= 0 ? pos[x.expert] : -1, py = y.expert >= 0 ? pos[y.expert] : -1;
+      return px != py ? px < py : x.row0 < y.row0;
+    });
+  }
   const auto t_copies = std::chrono::steady_clock::now();
 
   if (B > kDecodeMaxB) {
