@@ -158,7 +158,7 @@ def build_model(api, synth, torch, cfg, rank=0, world=1, max_batch=1, log=print,
             g, u, dn = synth.expert_weights(0, pl, e, S.d, S.I, device="cuda")
             bits = tuple(synth.bf16_bits(x) for x in (g, u, dn))
             ctx.load_expert(pl, e, *bits)
-            if pl == 0:
+            if pl == 0 and world == 1:   # only the single-GPU run times the oracle (cpu_baseline)
                 keep[e] = bits
     for i in range(L):
         for s in range(S.n_shared):
