@@ -448,7 +448,7 @@ void ControlPlane::make_plan(int j, const int32_t* ranking, Plan& out) const {
   const LayerState& l = layers[j];
   const int64_t cap_rows = (int64_t)U_b * I;
   int ycap = cfg.y_cap.empty() ? N : cfg.y_cap[j];
-  if (l.Y >= 0 && !getenv("MOEPIC_NO_SOLVER_YCAP")) ycap = std::min(ycap, l.Y);   // env: experiments
+  if (l.Y >= 0 && solver_y_cap) ycap = std::min(ycap, l.Y);
   int64_t used = 0;
   for (int y = 0; y < N; ++y) {
     int e = ranking[y];

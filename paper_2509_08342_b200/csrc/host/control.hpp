@@ -125,6 +125,7 @@ class ControlPlane {
   std::vector<LayerState> layers;
   CacheParams cfg;
   bool configured = false;
+  bool solver_y_cap = true;          // cap the plan at Alg. 1's Y_i (reading Q27); off only in experiments
   std::vector<double> V;             // current allocation (Alg. 1 state)
 
   ControlPlane(int L, int N, int K, int d, int I, int g, int U_b, int n_shared, int ep_rank,

@@ -297,7 +297,12 @@ struct moepic_ctx {
     feed_cancel.clear();
   }
 
-  bool host_timing = getenv("MOEPIC_HOST_TIMING") != nullptr;
+  // diagnostics switches, read once at create from the environment (tools only; no effect on
+  // results): MOEPIC_K1_TRACE / MOEPIC_K2_TRACE phase stamps, MOEPIC_HOST_TIMING host phases,
+  // MOEPIC_PF_CTA_PAIR = 0/1 forces the prefill CTA-pair choice (tests), MOEPIC_FEED_CHUNK_KB /
+  // MOEPIC_FEED_DEPTH / MOEPIC_NO_SOLVER_YCAP prefetch-feed experiments (scripts/feed_sweep.py)
+  bool k1_trace = false, k2_trace = false, host_timing = false;
+  int pf_cta_pair = -1;
   double ht[4] = {0, 0, 0, 0};
   double hc[2] = {0, 0};
   double hp[4] = {0, 0, 0, 0};
@@ -462,8 +467,13 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (cudaMemset(ctx->arena + lay.ticket, 0, 64) != cudaSuccess ||
       cudaMemset(ctx->arena + lay.rsel, 0, (size_t)desc->N * 16) != cudaSuccess)
     return bail(MOEPIC_ERUNTIME);
-  if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;   // experiments
-  if (const char* e = getenv("MOEPIC_FEED_DEPTH")) ctx->kFeedDepth = (size_t)atol(e);
+  if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;
+  if (const char* e = getenv("MOEPIC_FEED_DEPTH")) ctx->kFeedDepth = (size_t)std::min(atol(e), (long)moepic_ctx::kFeedRing);
+  if (const char* e = getenv("MOEPIC_PF_CTA_PAIR")) ctx->pf_cta_pair = atoi(e) ? 1 : 0;
+  ctx->k1_trace = getenv("MOEPIC_K1_TRACE") != nullptr;
+  ctx->k2_trace = getenv("MOEPIC_K2_TRACE") != nullptr;
+  ctx->host_timing = getenv("MOEPIC_HOST_TIMING") != nullptr;
+  ctx->cp->solver_y_cap = getenv("MOEPIC_NO_SOLVER_YCAP") == nullptr;
   ctx->slot_base.assign(desc->L, 0);
   ctx->ids_h.resize((size_t)desc->max_batch * desc->K);
   ctx->w_h.resize((size_t)desc->max_batch * desc->K);
@@ -758,7 +768,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
     kp.tstamp = ctx->tstamp(pe);
     kp.dbg = nullptr;
     static unsigned long long* dbg_buf = nullptr;   // MOEPIC_K2_TRACE: phase spans to stderr (tools)
-    const bool trace = getenv("MOEPIC_K2_TRACE") != nullptr;
+    const bool trace = ctx->k2_trace;
     if (trace) {
       if (!dbg_buf) cudaMalloc(&dbg_buf, 148 * 8 * 8);
       cudaMemsetAsync(dbg_buf, 0, 148 * 8 * 8, s);
@@ -860,7 +870,7 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_ROUTER);
   rp.tstamp = ctx->tstamp(pe);
   rp.dbg = nullptr;
-  if (getenv("MOEPIC_K1_TRACE")) {   // phase stamps per launch (tools): ring of 4096 x 8 u64
+  if (ctx->k1_trace) {   // phase stamps per launch (tools): ring of 4096 x 8 u64
     if (!ctx->k1dbg) {
       cudaMalloc(&ctx->k1dbg, 4096 * 64);
       cudaMemset(ctx->k1dbg, 0, 4096 * 64);
@@ -1010,9 +1020,8 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
     mt1 += table[e].mtiles;
     mt2 += 2 * ((table[e].mtiles + 1) / 2);
   }
-  const char* pair_env = getenv("MOEPIC_PF_CTA_PAIR");   // 0 / 1 forces both GEMMs (tests)
-  const int CGu = pair_env ? (atoi(pair_env) ? 2 : 1) : (mt2 * 10 <= mt1 * 11 ? 2 : 1);
-  const int CGd = pair_env ? (atoi(pair_env) ? 2 : 1) : 1;
+  const int CGu = ctx->pf_cta_pair >= 0 ? (ctx->pf_cta_pair ? 2 : 1) : (mt2 * 10 <= mt1 * 11 ? 2 : 1);
+  const int CGd = ctx->pf_cta_pair >= 0 ? (ctx->pf_cta_pair ? 2 : 1) : 1;
   auto ptiles = [&](int e, int CG) { return (int64_t)((table[e].mtiles + CG - 1) / CG); };
 
   auto run_group = [&](const std::vector<StepSeg>& g) -> moepic_status {
