@@ -24,8 +24,11 @@ struct CombineParamsCap {
 template <class P>
 __global__ void __launch_bounds__(kCombineWarps * 32) k3_combine(const __grid_constant__ P p) {
   __shared__ float4 red[kCombineWarps * 32];
+  extern __shared__ CombineSeg cs[];   // the segment table, walked per lane (see expert.cu)
   stamp_start(p.tstamp);
-  combine_block(blockIdx.x, p.segs, p.nsegs, p.ws, p.h, p.y, p.B, p.d, p.residual, red);
+  for (int i = threadIdx.x; i < p.nsegs; i += blockDim.x) cs[i] = p.segs[i];
+  __syncthreads();
+  combine_block(blockIdx.x, cs, p.nsegs, p.ws, p.h, p.y, p.B, p.d, p.residual, red);
   stamp_end(p.tstamp);
 }
 
@@ -37,7 +40,7 @@ static void launch_cap(const CombineParams& p, cudaStream_t s) {
   q.B = p.B; q.d = p.d; q.residual = p.residual; q.nsegs = p.nsegs; q.tstamp = p.tstamp;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   const int nblk = combine_blocks(p.B, p.d);
-  k3_combine<CombineParamsCap<CAP>><<<nblk, kCombineWarps * 32, 0, s>>>(q);
+  k3_combine<CombineParamsCap<CAP>><<<nblk, kCombineWarps * 32, (size_t)p.nsegs * sizeof(CombineSeg), s>>>(q);
 }
 
 __global__ void __launch_bounds__(256) k0_stage_in(uint4* __restrict__ dst, const uint4* __restrict__ src,

@@ -376,10 +376,15 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     if (dbg && tid == 0) dbg[3] = gtimer();
     // CTA c combines column blocks c, c + G, ... (combine_dev.cuh: 16 warps over the partials,
     // lanes over 32 float4 columns, fixed order); the K2 smem ring is free again here
+    // the segment table goes to shared memory first: the combine's lanes walk it at different
+    // positions, which the constant cache behind the kernel parameters would serialise
     float4* red = reinterpret_cast<float4*>(smem);
+    CombineSeg* cs = reinterpret_cast<CombineSeg*>(smem + kConsumerWarps * 32 * sizeof(float4));
+    for (int i = tid; i < p.ncomb; i += kThreads) cs[i] = p.comb[i];
+    __syncthreads();
     const int nblk = combine_blocks(p.B, d);
     for (int blk = blockIdx.x; blk < nblk; blk += G)
-      combine_block(blk, p.comb, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red);
+      combine_block(blk, cs, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red);
   }
   __syncthreads();
   if (dbg && tid == 0) dbg[4] = gtimer();
