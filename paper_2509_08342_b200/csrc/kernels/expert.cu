@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   const bool owns = c0 < d;
   float yacc[TB][CW];
   float hreg[TB][CW];
+  float hsum[TB], ylo[TB];   // Q4G64: sum of the thread's h columns; down-projection min terms
   float wgt[TB];
   float act_prev[RS][TB];
   int ntok = 0, prev_ntok = 0;
@@ -169,7 +170,28 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       }
     }
   };
+  // Q4G64 codes of part `part` as exact floats, with the group's scale and min: the dots then
+  // factor as min * sum(h) + scale * sum(code * h) (one FMA per weight instead of two)
+  auto load_codes = [&](const uint8_t* row, int part, float* q, float& sc, float& mn) {
+    const uint32_t prm =
+        *reinterpret_cast<const uint32_t*>(row + 3 * (d / 2) + (part * (d >> 6) + (c0 >> 6)) * 4);
+    sc = __uint_as_float(prm << 16);
+    mn = __uint_as_float(prm & 0xFFFF0000u);
+    uint32_t c;
+    if constexpr (CW == 8) c = *reinterpret_cast<const uint32_t*>(row + part * (d / 2) + (c0 >> 1));
+    else c = *reinterpret_cast<const uint16_t*>(row + part * (d / 2) + (c0 >> 1));
+#pragma unroll
+    for (int i = 0; i < CW; ++i) q[i] = __uint_as_float(0x4B000000u | ((c >> (4 * i)) & 15u)) - 8388608.0f;
+  };
   auto flush = [&](int s, int nt) {
+    if constexpr (Q4 != 0) {
+#pragma unroll
+      for (int t = 0; t < TB; ++t) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) yacc[t][c] += ylo[t];
+        ylo[t] = 0.f;
+      }
+    }
     const Seg& sg = p.segs[s];
     const int ci = (int)blockIdx.x - sg.cta_first;
     float* dst = p.ws + sg.ws_off + (int64_t)ci * nt * d;
@@ -190,21 +212,35 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
       if (r < prev_nr) {
-        float dn[CW];
-        load_part(prev_tile + (size_t)r * rowb, 2, dn);
+        if constexpr (Q4 != 0) {   // y += a * (min + code * scale) = a min + (a scale) code
+          float qd[CW], sc, mn;
+          load_codes(prev_tile + (size_t)r * rowb, 2, qd, sc, mn);
 #pragma unroll
-        for (int t = 0; t < TB; ++t) {
-          const float a = act_prev[r][t];
+          for (int t = 0; t < TB; ++t) {
+            const float a = act_prev[r][t], as = a * sc;
+            ylo[t] = fmaf(a, mn, ylo[t]);
 #pragma unroll
-          for (int c = 0; c < CW; c += 2) fma2(yacc[t][c], yacc[t][c + 1], a, a, dn[c], dn[c + 1]);
+            for (int c = 0; c < CW; c += 2) fma2(yacc[t][c], yacc[t][c + 1], as, as, qd[c], qd[c + 1]);
+          }
+        } else {
+          float dn[CW];
+          load_part(prev_tile + (size_t)r * rowb, 2, dn);
+#pragma unroll
+          for (int t = 0; t < TB; ++t) {
+            const float a = act_prev[r][t];
+#pragma unroll
+            for (int c = 0; c < CW; c += 2) fma2(yacc[t][c], yacc[t][c + 1], a, a, dn[c], dn[c + 1]);
+          }
         }
       }
     }
   };
 #pragma unroll
-  for (int t = 0; t < TB; ++t)
+  for (int t = 0; t < TB; ++t) {
+    ylo[t] = hsum[t] = 0.f;
 #pragma unroll
     for (int c = 0; c < CW; ++c) yacc[t][c] = 0.f;
+  }
 
   Tile it = start;
   for (int n = 0; it.row < r1; ++n) {
@@ -238,6 +274,12 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
 #pragma unroll
           for (int c = 0; c < CW; ++c) hreg[t][c] = 0.f;
         }
+        if constexpr (Q4 != 0) {
+          float hs = 0.f;
+#pragma unroll
+          for (int c = 0; c < CW; ++c) hs += hreg[t][c];
+          hsum[t] = hs;
+        }
       }
     }
     mbar_wait(&full[st], (n / kStagesV2) & 1);
@@ -252,7 +294,22 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     if (owns) {
 #pragma unroll
       for (int r = 0; r < RS; ++r) {
-        if (r < nr) {
+        if (r < nr && Q4 != 0) {   // min * sum(h) + scale * sum(code * h)
+          float qg[CW], qu[CW], sg, mg, su, mu;
+          load_codes(tile + (size_t)r * rowb, 0, qg, sg, mg);
+          load_codes(tile + (size_t)r * rowb, 1, qu, su, mu);
+#pragma unroll
+          for (int t = 0; t < TB; ++t) {
+            float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < CW; c += 2) {
+              fma2(a0, a1, qg[c], qg[c + 1], hreg[t][c], hreg[t][c + 1]);
+              fma2(b0, b1, qu[c], qu[c + 1], hreg[t][c], hreg[t][c + 1]);
+            }
+            pv[r * TB + t] += fmaf(sg, a0 + a1, mg * hsum[t]);
+            pv[RS * TB + r * TB + t] += fmaf(su, b0 + b1, mu * hsum[t]);
+          }
+        } else if (r < nr) {
           float g[CW], u[CW];
           load_part(tile + (size_t)r * rowb, 0, g);
           load_part(tile + (size_t)r * rowb, 1, u);

@@ -20,10 +20,11 @@ import synth  # noqa: E402
 from paper_2509_08342_b200 import api  # noqa: E402
 
 
-def run(shape, B, steps, L=2, theta=1.0, pcie_load=False, profile=True):
+def run(shape, B, steps, L=2, theta=1.0, pcie_load=False, profile=True, weights="bf16"):
     S = synth.SHAPES[shape]
     desc = api.model_desc(L, S.N, S.K, S.d, S.I, n_shared=S.n_shared, row_granule=64, max_batch=B,
-                          renorm_topk=S.renorm, L_host=1, v_e_max=L * S.N)
+                          renorm_topk=S.renorm, L_host=1, v_e_max=L * S.N,
+                          weight_format=api.M.Q4G64 if weights == "q4" else api.M.BF16)
     ctx = api.MoEpic(desc)
     for i in range(L):
         ctx.load_router(i, synth.bf16_bits(synth.router_weights(0, i, S.N, S.d)))
@@ -84,11 +85,12 @@ def main():
     ap.add_argument("--cases", default="mixtral:1,qwen3:1,qwen3:4,qwen3:16,deepseek:1")
     ap.add_argument("--pcie-load", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events (layer_us only)")
+    ap.add_argument("--weights", default="bf16", choices=["bf16", "q4"])
     args = ap.parse_args()
     for c in args.cases.split(","):
         shape, B = c.split(":")
-        print(json.dumps(run(shape, int(B), args.steps, pcie_load=args.pcie_load, profile=not args.no_profile)),
-              flush=True)
+        print(json.dumps(run(shape, int(B), args.steps, pcie_load=args.pcie_load, profile=not args.no_profile,
+                             weights=args.weights)), flush=True)
 
 
 if __name__ == "__main__":

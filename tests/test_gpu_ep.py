@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, B):
+def _worker(rank, world, port, q, B, fmt=0):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -35,8 +35,15 @@ def _worker(rank, world, port, q, B):
         from paper_2509_08342_b200 import api
         L, N, K, d, I = 2, 8, 2, 256, 512
         m = Model(L, N, K, d, I, n_shared=1, seed=17)
+        if fmt:   # Q4G64: the oracle sees the dequantised experts
+            from oracle import quant as Qz
+            from oracle import numeric as ON
+            deq = {k: Qz.dequantize_expert(Qz.quantize_expert(*w)) for k, w in m.experts.items()}
+            dsh = {k: Qz.dequantize_expert(Qz.quantize_expert(*w)) for k, w in m.shared.items()}
+            m.oracle_layer = lambda i, hb: ON.moe_layer(hb, m.routers[i], lambda e: deq[(i % m.L_host, e)], K,
+                                                        shared=[dsh[(i, s)] for s in range(m.n_shared)])
         desc = api.model_desc(L, N, K, d, I, n_shared=1, row_granule=64, max_batch=B, v_e_max=8.0,
-                              ep_rank=rank, ep_size=world)
+                              ep_rank=rank, ep_size=world, weight_format=fmt)
         ctx = api.MoEpic(desc)
         m.load_into(ctx)
         ctx.configure(v_e=2.0, seed=1)
@@ -68,14 +75,14 @@ def _worker(rank, world, port, q, B):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B", [1, 3, 64])
-def test_ep_two_ranks_one_gpu(B):
+@pytest.mark.parametrize("B,fmt", [(1, 0), (3, 0), (64, 0), (3, 1)])
+def test_ep_two_ranks_one_gpu(B, fmt):
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, B)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, B, fmt)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=600) for _ in ps)
