@@ -47,6 +47,10 @@ CONFIGS = {
 }
 
 
+# attention stand-in heads (Hq, Hkv), head dim 128: Mixtral and Qwen3-30B-A3B public GQA configs;
+# DeepSeek-V2-Lite uses MLA, stood in for by 16 full heads
+ATTN_HEADS = {"mixtral": (32, 8), "qwen3": (32, 4), "deepseek": (16, 16), "toy": (4, 2)}
+
 # NEXT-1 ablation modes on the same engine
 MODES = {
     "moepic": {},                                                   # LCP + SP + CCA (Alg. 1 if adaptive)
@@ -241,12 +245,33 @@ def run_ours(args, log):
     stream = torch.cuda.Stream()
     F = api.M.FUSE_PREDICT
 
+    # attention stand-in (--attention S): GQA decode over a KV cache of S
+    # positions before every MoE layer (the paper's Att^i, Eq. 1), caches aliased over L_host layers
+    attn = None
+    if args.attention > 0 and not cfg.get("prefill"):
+        Hq, Hkv = ATTN_HEADS[cfg["shape"]]
+        gen = torch.Generator(device="cuda").manual_seed(7)
+        kc = [torch.randn(B, args.attention, Hkv, 128, generator=gen, device="cuda").to(torch.bfloat16)
+              for _ in range(cfg["L_host"])]
+        vc = [torch.randn(B, args.attention, Hkv, 128, generator=gen, device="cuda").to(torch.bfloat16)
+              for _ in range(cfg["L_host"])]
+        qa = torch.randn(B, Hq, 128, generator=gen, device="cuda").to(torch.bfloat16)
+        oa = torch.empty(B, Hq, 128, dtype=torch.float32, device="cuda")
+        attn_op = api.Attention(B, args.attention, Hq, Hkv)
+
+        def attn(i):
+            attn_op(qa, kc[i % cfg["L_host"]], vc[i % cfg["L_host"]], args.attention, oa, stream=stream)
+
     def token(t):
         for i in range(L):
+            if attn:
+                attn(i)
             ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=F, trace=False)
 
     def token_ep(t):
         for i in range(L):
+            if attn:
+                attn(i)
             ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=F, trace=False)
             with torch.cuda.stream(stream):
                 dist.all_reduce(y)      # EP combine: sum of per-rank partial outputs
@@ -282,6 +307,20 @@ def run_ours(args, log):
         step = token_ep_prefill
     else:
         step = token_ep if world > 1 else token
+    t_att = 0.0   # ms per layer of the attention stand-in (Alg. 1's T_att)
+    if attn:
+        for i in range(L):
+            attn(i)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(50_000_000)   # hold the stream while the host enqueues: GPU time only
+        a0.record(stream)
+        for i in range(4 * L):
+            attn(i)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        t_att = a0.elapsed_time(a1) / (4 * L)
+        log(f"[bench] attention stand-in {t_att * 1e3:.1f} us per layer (S = {args.attention})")
     solved = None
     if adapt_tokens:
         # Alg. 1 outer loop: run 2 tau tokens on the uniform theta = 0.5 layout, profile
@@ -297,7 +336,7 @@ def run_ours(args, log):
         t_load = U_e / (pcie * 1e9) * 1e3                          # ms per full expert
         t_moe = k2w["total_ms"] / (adapt_tokens * L)               # ms of expert compute per layer-step
         t0 = time.time()
-        solved = ctx.configure(use_solver=True, t_att=0.0, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
+        solved = ctx.configure(use_solver=True, t_att=t_att, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
                                zeta=0.01, **{k: v for k, v in base_cfg.items() if k != "theta_i"})
         log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(solved['theta_eff_i']):.2f}.."
             f"{max(solved['theta_eff_i']):.2f}, C {min(solved['C_i'])}..{max(solved['C_i'])}")
@@ -428,6 +467,8 @@ def run_ours(args, log):
                        else "all_reduce(y) of the per-rank partial outputs"),
                    "v_e_experts": base_cfg["v_e"], "theta": base_cfg["theta_i"][0], "mode": args.mode,
                    "weights": args.weights,
+                   "attention": None if not attn else {"kv_positions": args.attention, "heads": ATTN_HEADS[cfg["shape"]],
+                                                       "us_per_layer": round(t_att * 1e3, 2)},
                    "policy": MODES[args.mode].get("policy", "LCP"), "prefetch": base_cfg.get("prefetch", True),
                    "y_cap": S.K * B,
                    "alg1": None if solved is None else {"tau_tokens": args.tau, "theta_eff_min": min(solved["theta_eff_i"]),
@@ -582,6 +623,9 @@ def main():
     ap.add_argument("--mode", default="moepic", choices=sorted(MODES), help="ablation mode (SURVEY §8(f) NEXT-1)")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="time the step without the per-kernel CUDA events (roofline fields then empty)")
+    ap.add_argument("--attention", type=int, default=0,
+                    help="KV positions of the attention stand-in run before every MoE layer (0 = MoE-only "
+                         "stack, the default metric); its time is Alg. 1's T_att")
     ap.add_argument("--weights", default="bf16", choices=["bf16", "q4"],
                     help="expert storage: bf16 (default, the headline) or q4 = Q4G64 low-bit experts "
                          "(SURVEY §8(f) NEXT-3; a reduced-precision mode, never the headline)")

@@ -214,3 +214,22 @@ def predicted_ranking(pred_logits: np.ndarray, K: int) -> np.ndarray:
     mx = pred_logits.max(axis=0)
     order = sorted(range(N), key=lambda j: (-c[j], -mx[j], j))
     return np.array(order, dtype=np.int32)
+
+
+def attention_decode(q_bits, k_bits, v_bits, S):
+    """Attention stand-in (Att^i of Eq. 1): grouped-query attention
+    of B decode tokens over the first S positions of a KV cache, fp64.
+    q [B][Hq][dh], k / v [B][S_max][Hkv][dh] (bf16 bits); head h reads kv head h // (Hq / Hkv).
+    out[b][h] = sum_s softmax_s(q . k_s / sqrt(dh)) v_s."""
+    q, k, v = bf16_to_f64(q_bits), bf16_to_f64(k_bits), bf16_to_f64(v_bits)
+    B, Hq, dh = q.shape
+    Hkv = k.shape[2]
+    G = Hq // Hkv
+    out = np.zeros((B, Hq, dh))
+    for b in range(B):
+        for h in range(Hq):
+            kk, vv = k[b, :S, h // G], v[b, :S, h // G]
+            sc = kk @ q[b, h] / np.sqrt(dh)
+            p = np.exp(sc - sc.max())
+            out[b, h] = (p / p.sum()) @ vv
+    return out

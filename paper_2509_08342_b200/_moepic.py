@@ -95,6 +95,11 @@ _sig = {
     "moepic_get_counters": (C.c_int, [_ctxp, C.POINTER(moepic_counters)]),
     "moepic_profile": (C.c_int, [_ctxp, C.c_int32]),
     "moepic_profile_read": (C.c_int, [_ctxp, C.c_int32, C.POINTER(moepic_kernel_stats)]),
+    "moepic_attention_ws_bytes": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.POINTER(C.c_size_t)]),
+    "moepic_attention_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                          C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t,
+                                          C.c_void_p]),
     "moepic_last_error": (C.c_char_p, [_ctxp]),
     "moepic_destroy": (None, [_ctxp]),
     "moepic_hostsim_create": (C.c_int, [C.POINTER(moepic_model_desc), C.POINTER(_ctxp)]),

@@ -272,3 +272,24 @@ class HostSim:
         n = C.c_int32()
         self._err(M.moepic_hostsim_cached(self.h, layer, _ptr(out, C.c_int32), C.byref(n)), "moepic_hostsim_cached")
         return set(out[:n.value].tolist())
+
+
+class Attention:
+    """moepic_attention_decode (attention stand-in) with its scratch held in a
+    torch tensor.  q bf16 [B][Hq][128], caches bf16 [B][S_max][Hkv][128] (cuda)."""
+
+    def __init__(self, B, S_max, Hq, Hkv, dh=128, device="cuda"):
+        import torch
+        n = C.c_size_t()
+        _check(M.moepic_attention_ws_bytes(B, S_max, Hq, Hkv, dh, C.byref(n)), "moepic_attention_ws_bytes")
+        self.ws = torch.empty(int(n.value), dtype=torch.uint8, device=device)
+        self.B, self.S_max, self.Hq, self.Hkv, self.dh = B, S_max, Hq, Hkv, dh
+
+    def __call__(self, q, k_cache, v_cache, S, out, stream=None):
+        sp = C.c_void_p(stream.cuda_stream if stream is not None else None)
+        _check(M.moepic_attention_decode(C.c_void_p(q.data_ptr()), C.c_void_p(k_cache.data_ptr()),
+                                         C.c_void_p(v_cache.data_ptr()), q.shape[0], S, k_cache.shape[1],
+                                         self.Hq, self.Hkv, self.dh, C.c_void_p(out.data_ptr()),
+                                         C.c_void_p(self.ws.data_ptr()), self.ws.numel(), sp),
+               "moepic_attention_decode")
+        return out

@@ -22,7 +22,8 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu", "kernels/prefill.cu"]
+CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu", "kernels/prefill.cu",
+              "kernels/attention.cu"]
 CXX_SOURCES = ["host/control.cpp", "moepic_api.cpp"]
 HEADERS = ["kernels/kernels.hpp", "kernels/device_utils.cuh", "kernels/prefill.hpp", "host/control.hpp", "../../include/moepic.h", "../../include/moepic_hostsim.h"]
 

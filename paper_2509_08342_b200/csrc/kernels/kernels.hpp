@@ -111,6 +111,19 @@ void launch_combine(const CombineParams& p, cudaStream_t s);
 // engine's multi-MB chunks on the host->device copy engine.  bytes % 16 == 0.
 void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
 
+// Attention stand-in (attention.cu): GQA decode over a KV cache [B][S_max][Hkv][dh], dh = 128.
+constexpr int kAttnChunk = 128;   // cache positions per split: one CTA (4 warps x 32) per split and kv head
+struct AttnParams {
+  const uint16_t* q;      // [B][Hq][dh] bf16
+  const uint16_t* k;      // [B][S_max][Hkv][dh] bf16
+  const uint16_t* v;
+  float* out;             // [B][Hq][dh] fp32
+  float* ws;              // [B][Hq][splits][dh + 2] partials
+  int B, S, S_max, Hq, Hkv, splits;
+};
+int attn_splits(int S);
+bool launch_attention(const AttnParams& p, cudaStream_t s);   // false: unsupported group size
+
 bool kernels_init(char* err, size_t errlen);  // sets smem attributes; returns false on failure
 
 }  // namespace moepic

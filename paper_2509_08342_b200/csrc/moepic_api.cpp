@@ -1510,6 +1510,33 @@ moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_
   return MOEPIC_OK;
 }
 
+moepic_status moepic_attention_ws_bytes(int32_t B, int32_t S, int32_t Hq, int32_t Hkv, int32_t dh, size_t* bytes) {
+  if (!bytes || B < 1 || S < 1 || Hq < 1 || Hkv < 1 || dh != 128) return MOEPIC_EINVAL;
+  *bytes = (size_t)B * Hq * attn_splits(S) * (dh + 2) * sizeof(float);
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_attention_decode(const void* q, const void* k_cache, const void* v_cache, int32_t B,
+                                      int32_t S, int32_t S_max, int32_t Hq, int32_t Hkv, int32_t dh,
+                                      float* out, void* ws, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  if (moepic_attention_ws_bytes(B, S, Hq, Hkv, dh, &need) != MOEPIC_OK) return MOEPIC_EINVAL;
+  if (!q || !k_cache || !v_cache || !out || !ws || S > S_max || Hq % Hkv != 0 || ws_bytes < need) return MOEPIC_EINVAL;
+  for (const void* ptr : {q, k_cache, v_cache, (const void*)out, (const void*)ws})
+    if (reinterpret_cast<uintptr_t>(ptr) & 7) return MOEPIC_EINVAL;
+  const int G = Hq / Hkv;
+  if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16) return MOEPIC_EINVAL;
+  AttnParams p{};
+  p.q = static_cast<const uint16_t*>(q);
+  p.k = static_cast<const uint16_t*>(k_cache);
+  p.v = static_cast<const uint16_t*>(v_cache);
+  p.out = out;
+  p.ws = static_cast<float*>(ws);
+  p.B = B; p.S = S; p.S_max = S_max; p.Hq = Hq; p.Hkv = Hkv; p.splits = attn_splits(S);
+  if (!launch_attention(p, static_cast<cudaStream_t>(stream))) return MOEPIC_EINVAL;
+  return cudaGetLastError() == cudaSuccess ? MOEPIC_OK : MOEPIC_ERUNTIME;
+}
+
 const char* moepic_last_error(const moepic_ctx* ctx) { return ctx ? ctx->err.c_str() : "ctx is NULL"; }
 
 void moepic_destroy(moepic_ctx* ctx) {
