@@ -11,6 +11,8 @@ for c in qwen3 deepseek toy; do
 done
 python bench.py --config mixtral_prefill --steps 4 --warmup 3 > $OUT/bench_mixtral_prefill.json 2> $OUT/bench_mixtral_prefill.log
 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference_mixtral.json 2> $OUT/bench_reference.log
+python bench.py --weights q4 --steps 32 --warmup 3 --no-cpu-baseline > $OUT/bench_mixtral_q4.json 2> $OUT/bench_mixtral_q4.log
+python bench.py --attention 4096 --steps 16 --warmup 3 --no-cpu-baseline > $OUT/bench_mixtral_attention.json 2> $OUT/bench_mixtral_attention.log
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_bench.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/launches_bench.log 2>&1
 for c in mixtral qwen3 deepseek; do
@@ -19,6 +21,8 @@ for c in mixtral qwen3 deepseek; do
 done
 ncu --set full --clock-control none --import-source on -k regex:k1_router -s 5 -c 2 -f -o $OUT/k1_qwen3 \
     python scripts/k2_bench.py --cases qwen3:1 --steps 3 > $OUT/ncu_k1_qwen3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_attn -s 64 -c 2 -f -o $OUT/attn_mixtral \
+    python bench.py --attention 4096 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-adapt > $OUT/ncu_attn.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k2_split_expert -s 300 -c 3 -f -o $OUT/k2_step_mixtral \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-adapt > $OUT/ncu_k2_step.log 2>&1
 ls -la $OUT

@@ -104,3 +104,28 @@ def test_invalid_configs_rejected():
             hs.configure(**bad)
     with pytest.raises(api.MoEpicError):
         api.HostSim(api.model_desc(2, 8, 8, 64, 128, row_granule=16))   # K must be < N
+
+
+# randomised sweep (hypothesis): shapes, budgets, split ratios, policies, prefetch, buffer size,
+# batch, shared experts and an Alg. 1 reconfiguration midway — every trace bit-exact
+try:
+    from hypothesis import given, settings, strategies as st, HealthCheck
+except ImportError:   # pragma: no cover
+    given = None
+
+if given is not None:
+    @settings(max_examples=80, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+    @given(L=st.integers(1, 4), N=st.sampled_from([4, 8, 16, 32]), kfrac=st.floats(0.05, 0.6),
+           I=st.sampled_from([64, 128, 256]), B=st.integers(1, 4), policy=st.sampled_from([P.LCP, P.LRU, P.LFU, P.RND]),
+           prefetch=st.booleans(), vfrac=st.floats(0.0, 1.0), theta=st.sampled_from([None, 0.25, 0.5, 0.75, 1.0]),
+           ub_extra=st.integers(0, 2), n_shared=st.integers(0, 2), solver=st.booleans(), seed=st.integers(0, 10 ** 6))
+    def test_random_configurations(L, N, kfrac, I, B, policy, prefetch, vfrac, theta, ub_extra, n_shared, solver,
+                                   seed):
+        K = max(1, min(N - 1, int(round(kfrac * N))))
+        v_e = round(vfrac * L * N, 2)
+        kw = dict(v_e=v_e, policy=policy, prefetch=prefetch, seed=seed % 97)
+        if theta is not None:
+            kw["theta_i"] = [theta] * L
+        skw = dict(use_solver=True, t_att=15.0, t_moe=30.0, t_head=5.0, t_load_exp=45.0, zeta=0.05)
+        _run_pair(L, N, K, 64, I, 16, K + ub_extra, B, kw, T=24, seed=seed, n_shared=n_shared,
+                  solver_at=8 if solver else None, solver_kw=skw)
