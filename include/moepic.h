@@ -257,7 +257,7 @@ moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_
  * positions s < S of caches holding S_max positions.  Device pointers: q bf16 [B][Hq][dh],
  * k_cache / v_cache bf16 [B][S_max][Hkv][dh], out fp32 [B][Hq][dh], ws caller-owned scratch of
  * moepic_attention_ws_bytes bytes.  Enqueued on `stream` (cudaStream_t as void*).  EINVAL unless
- * dh == 128, Hq % Hkv == 0 with G in {1, 2, 4, 8, 16}, 1 <= S <= S_max, B >= 1, pointers non-NULL
+ * dh == 128, Hq % Hkv == 0 with G in {1, 2, 4, 8, 16}, 1 <= S <= S_max <= 131072, B >= 1, pointers non-NULL
  * and 8-byte aligned, ws large enough; ERUNTIME if the launch fails.                          */
 moepic_status moepic_attention_ws_bytes(int32_t B, int32_t S, int32_t Hq, int32_t Hkv, int32_t dh, size_t* bytes);
 moepic_status moepic_attention_decode(const void* q, const void* k_cache, const void* v_cache, int32_t B,

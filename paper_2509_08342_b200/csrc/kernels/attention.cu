@@ -134,23 +134,54 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn_split(AttnParams p) {
 }
 
 __global__ void __launch_bounds__(kAttnDh) k_attn_merge(AttnParams p) {
+  // the splits' (m, l) are read in parallel (one thread each) and turned into weights once; then
+  // every thread (one dim) sums its column with independent loads
+  constexpr int kMaxSplits = 1024;   // S <= 131072 positions
+  __shared__ float sc[kMaxSplits];
+  __shared__ float sL;
   const int h = blockIdx.x, b = blockIdx.y, i = threadIdx.x;
   const float* part = p.ws + ((size_t)b * p.Hq + h) * p.splits * (kAttnDh + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < p.splits; ++s) M = fmaxf(M, part[(size_t)s * (kAttnDh + 2)]);
-  float L = 0.f, a = 0.f;
-  for (int s = 0; s < p.splits; ++s) {
-    const float* ps = part + (size_t)s * (kAttnDh + 2);
-    const float c = ps[0] == -INFINITY ? 0.f : __expf(ps[0] - M);
-    L += ps[1] * c;
-    a += ps[2 + i] * c;
+  float mloc = -INFINITY;
+  for (int sp = i; sp < p.splits; sp += kAttnDh) mloc = fmaxf(mloc, part[(size_t)sp * (kAttnDh + 2)]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+  __shared__ float swm[kAttnDh / 32];
+  if ((i & 31) == 0) swm[i >> 5] = mloc;
+  __syncthreads();
+  float M = swm[0];
+#pragma unroll
+  for (int w = 1; w < kAttnDh / 32; ++w) M = fmaxf(M, swm[w]);
+  for (int sp = i; sp < p.splits; sp += kAttnDh) {
+    const float m0 = part[(size_t)sp * (kAttnDh + 2)];
+    sc[sp] = m0 == -INFINITY ? 0.f : __expf(m0 - M);
   }
-  p.out[((size_t)b * p.Hq + h) * kAttnDh + i] = a / L;
+  __syncthreads();
+  if (i == 0) {   // sum of l in split order (fixed order)
+    float L = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) L += part[(size_t)sp * (kAttnDh + 2) + 1] * sc[sp];
+    sL = L;
+  }
+  float a = 0.f;
+#pragma unroll 8
+  for (int sp = 0; sp < p.splits; ++sp) a += part[(size_t)sp * (kAttnDh + 2) + 2 + i] * sc[sp];
+  __syncthreads();
+  p.out[((size_t)b * p.Hq + h) * kAttnDh + i] = a / sL;
 }
 
 template <int G>
 static void launch_g(const AttnParams& p, cudaStream_t s) {
   k_attn_split<G><<<dim3(p.splits, p.Hkv, p.B), kAttnWarps * 32, 0, s>>>(p);
+}
+
+// the decode step alternates these kernels with K2 (~200 KB of shared memory): asking for the
+// maximum carveout keeps the SM's L1 / shared split unchanged between them
+cudaError_t attention_init() {
+  cudaError_t e = cudaSuccess, r;
+  const void* fns[] = {(const void*)k_attn_split<1>, (const void*)k_attn_split<2>, (const void*)k_attn_split<4>,
+                       (const void*)k_attn_split<8>, (const void*)k_attn_split<16>, (const void*)k_attn_merge};
+  for (const void* f : fns)
+    if ((r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) e = r;
+  return e;
 }
 
 bool launch_attention(const AttnParams& p, cudaStream_t s) {

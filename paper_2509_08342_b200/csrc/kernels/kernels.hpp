@@ -123,6 +123,7 @@ struct AttnParams {
 };
 int attn_splits(int S);
 bool launch_attention(const AttnParams& p, cudaStream_t s);   // false: unsupported group size
+cudaError_t attention_init();
 
 bool kernels_init(char* err, size_t errlen);  // sets smem attributes; returns false on failure
 

@@ -1511,7 +1511,7 @@ moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_
 }
 
 moepic_status moepic_attention_ws_bytes(int32_t B, int32_t S, int32_t Hq, int32_t Hkv, int32_t dh, size_t* bytes) {
-  if (!bytes || B < 1 || S < 1 || Hq < 1 || Hkv < 1 || dh != 128) return MOEPIC_EINVAL;
+  if (!bytes || B < 1 || S < 1 || S > 1024 * kAttnChunk || Hq < 1 || Hkv < 1 || dh != 128) return MOEPIC_EINVAL;
   *bytes = (size_t)B * Hq * attn_splits(S) * (dh + 2) * sizeof(float);
   return MOEPIC_OK;
 }
@@ -1526,6 +1526,8 @@ moepic_status moepic_attention_decode(const void* q, const void* k_cache, const 
     if (reinterpret_cast<uintptr_t>(ptr) & 7) return MOEPIC_EINVAL;
   const int G = Hq / Hkv;
   if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16) return MOEPIC_EINVAL;
+  static const bool attrs_ok = attention_init() == cudaSuccess;   // context-free entry: set once
+  (void)attrs_ok;
   AttnParams p{};
   p.q = static_cast<const uint16_t*>(q);
   p.k = static_cast<const uint16_t*>(k_cache);

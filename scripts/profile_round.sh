@@ -25,4 +25,12 @@ ncu --set full --clock-control none --import-source on -k regex:k_attn -s 64 -c 
     python bench.py --attention 4096 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-adapt > $OUT/ncu_attn.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k2_split_expert -s 300 -c 3 -f -o $OUT/k2_step_mixtral \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-adapt > $OUT/ncu_k2_step.log 2>&1
+# summaries on the box; the reports themselves stay there (gpurun copies back <= 64 MiB)
+python scripts/ncu_summary.py --launches $OUT/launches_bench.csv > $OUT/summary_launches.md 2>&1
+for r in k2_mixtral k2_qwen3 k2_deepseek k2_step_mixtral k1_qwen3 attn_mixtral; do
+  python scripts/ncu_summary.py $OUT/$r.ncu-rep > $OUT/summary_$r.md 2>&1
+done
+python scripts/ncu_traffic.py --out $OUT/ncu_traffic.json --k2 mixtral=$OUT/k2_mixtral.ncu-rep qwen3=$OUT/k2_qwen3.ncu-rep \
+    deepseek=$OUT/k2_deepseek.ncu-rep --k2-bytes mixtral=704660000 qwen3=75530000 deepseek=138440000 > /dev/null 2>&1
+rm -f $OUT/*.ncu-rep $OUT/launches_bench.csv
 ls -la $OUT
