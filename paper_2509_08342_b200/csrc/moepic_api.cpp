@@ -306,6 +306,8 @@ struct moepic_ctx {
   double ht[4] = {0, 0, 0, 0};
   double hc[2] = {0, 0};
   double hp[4] = {0, 0, 0, 0};
+  double hf[5] = {0, 0, 0, 0, 0};
+  uint64_t hf_n = 0;
   uint64_t hc_n = 0;
   uint64_t ht_n = 0;
   unsigned long long* k1dbg = nullptr;   // MOEPIC_K1_TRACE ring (tools)
@@ -942,18 +944,32 @@ static moepic_status issue_plan(moepic_ctx* ctx, Plan& plan, int buf) {
 // Routing of the plan's target layer is known: drop the unissued chunks of experts it did not
 // activate, issue everything else, and mark the point the plan's segments wait for.
 static moepic_status finish_plan(moepic_ctx* ctx, const Plan& plan, const StepResult& res) {
+  const auto f0 = std::chrono::steady_clock::now();
   if (ctx->cancel_prefetch) {
     std::vector<char> act(ctx->desc.N, 0);
     for (int e : res.A) act[e] = 1;
     for (size_t k = 0; k < plan.items.size(); ++k)
       if (!act[plan.items[k].expert]) ctx->feed_cancel[k] = 1;
   }
+  const auto f1 = std::chrono::steady_clock::now();
+  const size_t issued0 = ctx->feed_next;
   if (!ctx->feed_pump((size_t)-1)) {
     ctx->poisoned = true;
     return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch copy: %s", cudaGetErrorString(cudaGetLastError()));
   }
+  const auto f2 = std::chrono::steady_clock::now();
+  const size_t issued = ctx->feed_next - issued0;
   ctx->feed_drop();
   if (!plan.items.empty()) CK(cudaEventRecord(ctx->ev_plan[plan.buf], ctx->copy));   // gB waits on it
+  if (ctx->host_timing) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    ctx->hf[0] += us(f0, f1);
+    ctx->hf[1] += us(f1, f2);
+    ctx->hf[2] += us(f2, std::chrono::steady_clock::now());
+    ctx->hf[3] += (double)issued;
+    ctx->hf[4] += (double)plan.items.size();
+    ctx->hf_n++;
+  }
   return MOEPIC_OK;
 }
 
@@ -1551,6 +1567,10 @@ void moepic_destroy(moepic_ctx* ctx) {
   if (ctx->ht_n)
     fprintf(stderr, "[hosttiming] classify %.1f, finish_plan %.1f, pass 1 %.1f, commit %.1f us\n", ctx->hp[0] / ctx->ht_n,
             ctx->hp[1] / ctx->ht_n, ctx->hp[2] / ctx->ht_n, ctx->hp[3] / ctx->ht_n);
+  if (ctx->hf_n)
+    fprintf(stderr, "[hosttiming] finish_plan x%llu: cancel %.1f, pump %.1f (%.2f chunks issued, %.2f items), drop+record %.1f us\n",
+            (unsigned long long)ctx->hf_n, ctx->hf[0] / ctx->hf_n, ctx->hf[1] / ctx->hf_n, ctx->hf[3] / ctx->hf_n,
+            ctx->hf[4] / ctx->hf_n, ctx->hf[2] / ctx->hf_n);
   if (ctx->hc_n)
     fprintf(stderr, "[hosttiming] %llu copies: stream waits %.1f us, cudaMemcpyAsync %.1f us per copy\n",
             (unsigned long long)ctx->hc_n, ctx->hc[0] / ctx->hc_n, ctx->hc[1] / ctx->hc_n);
