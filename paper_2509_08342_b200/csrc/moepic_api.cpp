@@ -306,7 +306,7 @@ struct moepic_ctx {
   double ht[4] = {0, 0, 0, 0};
   double hc[2] = {0, 0};
   double hp[4] = {0, 0, 0, 0};
-  double hf[5] = {0, 0, 0, 0, 0};
+  double hf[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t hf_n = 0;
   uint64_t hc_n = 0;
   uint64_t ht_n = 0;
@@ -953,6 +953,10 @@ static moepic_status finish_plan(moepic_ctx* ctx, const Plan& plan, const StepRe
   }
   const auto f1 = std::chrono::steady_clock::now();
   const size_t issued0 = ctx->feed_next;
+  const uint64_t copies0 = ctx->ctr.h2d_copies;
+  const size_t infl0 = ctx->feed_inflight.size();
+  int act_items = 0;
+  for (size_t k = 0; k < plan.items.size(); ++k) act_items += ctx->feed_cancel.empty() || !ctx->feed_cancel[k];
   if (!ctx->feed_pump((size_t)-1)) {
     ctx->poisoned = true;
     return fail(&ctx->err, MOEPIC_ERUNTIME, "prefetch copy: %s", cudaGetErrorString(cudaGetLastError()));
@@ -968,6 +972,10 @@ static moepic_status finish_plan(moepic_ctx* ctx, const Plan& plan, const StepRe
     ctx->hf[2] += us(f2, std::chrono::steady_clock::now());
     ctx->hf[3] += (double)issued;
     ctx->hf[4] += (double)plan.items.size();
+    ctx->hf[5] += (double)(ctx->ctr.h2d_copies - copies0);
+    ctx->hf[6] += (double)infl0;
+    ctx->hf[7] += (double)act_items;
+    ctx->hf[8] += (double)ctx->feed.size();
     ctx->hf_n++;
   }
   return MOEPIC_OK;
@@ -1568,9 +1576,11 @@ void moepic_destroy(moepic_ctx* ctx) {
     fprintf(stderr, "[hosttiming] classify %.1f, finish_plan %.1f, pass 1 %.1f, commit %.1f us\n", ctx->hp[0] / ctx->ht_n,
             ctx->hp[1] / ctx->ht_n, ctx->hp[2] / ctx->ht_n, ctx->hp[3] / ctx->ht_n);
   if (ctx->hf_n)
-    fprintf(stderr, "[hosttiming] finish_plan x%llu: cancel %.1f, pump %.1f (%.2f chunks issued, %.2f items), drop+record %.1f us\n",
-            (unsigned long long)ctx->hf_n, ctx->hf[0] / ctx->hf_n, ctx->hf[1] / ctx->hf_n, ctx->hf[3] / ctx->hf_n,
-            ctx->hf[4] / ctx->hf_n, ctx->hf[2] / ctx->hf_n);
+    fprintf(stderr, "[hosttiming] finish_plan x%llu: cancel %.1f, pump %.1f (feed %.2f chunks, %.2f walked, %.2f copied, "
+            "%.2f in flight before; %.2f items, %.2f kept), drop+record %.1f us\n",
+            (unsigned long long)ctx->hf_n, ctx->hf[0] / ctx->hf_n, ctx->hf[1] / ctx->hf_n, ctx->hf[8] / ctx->hf_n,
+            ctx->hf[3] / ctx->hf_n, ctx->hf[5] / ctx->hf_n, ctx->hf[6] / ctx->hf_n, ctx->hf[4] / ctx->hf_n,
+            ctx->hf[7] / ctx->hf_n, ctx->hf[2] / ctx->hf_n);
   if (ctx->hc_n)
     fprintf(stderr, "[hosttiming] %llu copies: stream waits %.1f us, cudaMemcpyAsync %.1f us per copy\n",
             (unsigned long long)ctx->hc_n, ctx->hc[0] / ctx->hc_n, ctx->hc[1] / ctx->hc_n);
