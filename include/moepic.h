@@ -65,7 +65,9 @@ typedef struct moepic_ctx moepic_ctx;
 /* Model shape (Table 2).  Invariants (EINVAL otherwise):
  *   1 <= K < N; L >= 1; d % 8 == 0 and d >= 8; I % row_granule == 0;
  *   row_granule % 16 == 0; buffer_experts >= K (U_b); 1 <= max_batch <= 4096;
- *   1 <= L_host <= L; 0 <= ep_rank < ep_size; N % ep_size == 0; tp fields as documented below. */
+ *   1 <= L_host <= L; 0 <= ep_rank < ep_size; N % ep_size == 0; tp fields as documented below;
+ *   max_batch > 32 (prefill) additionally needs d % 256 == 0, N + n_shared <= 136 and
+ *   row_granule, I / tp_size multiples of 64.                                                  */
 typedef struct {
   int32_t L, N, K, d, I;  /* layers, routed experts per layer, top-K, hidden, intermediate     */
   int32_t n_shared;       /* shared experts per layer: always resident, weight 1, unsplit (Q6) */

@@ -71,6 +71,8 @@ std::string validate_desc(const moepic_model_desc* d) {
   if (d->weight_format != MOEPIC_BF16 && d->weight_format != MOEPIC_Q4G64) return "weight_format invalid";
   if (d->weight_format == MOEPIC_Q4G64 && (d->d % 64 != 0 || d->max_batch > kDecodeMaxB))
     return "Q4G64 experts need d % 64 == 0 and max_batch <= 32";
+  if (d->max_batch > kDecodeMaxB && (d->row_granule % 64 != 0 || (d->I / d->tp_size) % 64 != 0))
+    return "prefill batches (max_batch > 32) need row_granule and I / tp_size to be multiples of 64 (GEMM K tiles)";
   return "";
 }
 

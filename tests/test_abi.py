@@ -49,7 +49,8 @@ def test_arena_bytes_and_desc_validation():
     assert 128 * 352321536 // 4 < nt.value < n.value // 3
     for bad in (dict(K=8), dict(d=4100), dict(I=1000), dict(max_batch=8192), dict(L_host=40),
                 dict(tp_size=0), dict(tp_rank=2, tp_size=2), dict(tp_size=3),
-                dict(tp_size=2, ep_size=2), dict(I=14336 + 64, tp_size=2)):
+                dict(tp_size=2, ep_size=2), dict(I=14336 + 64, tp_size=2),
+                dict(max_batch=64, I=14336 + 32, row_granule=32)):   # prefill K tiles need 64-row granules
         kw = dict(L=32, N=8, K=2, d=4096, I=14336, max_batch=1, v_e_max=128, L_host=2)
         kw.update(bad)
         if "I" in bad and "tp_size" in bad:   # I = 14400 = 225 granules: odd, so no even split
