@@ -34,7 +34,7 @@ __host__ __device__ inline int combine_blocks(int B, int d) {
 // Must be called by all kCombineWarps * 32 threads of the block; `red` is 16 * 32 float4 of smem.
 __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, int nsegs, const float* ws,
                                               const uint16_t* h, float* y, int B, int d, int residual,
-                                              float4* red) {
+                                              float4* red, unsigned long long* dbg = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d4 = d >> 2;
   const int CB = combine_cb(B, d);
@@ -53,6 +53,7 @@ __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, i
   int total = 0;
   for (int s = 0; s < nsegs; ++s)
     if (segs[s].tok_mask & bit) total += segs[s].nchunks;
+  if (dbg && threadIdx.x == 0) dbg[5] = gtimer();
   int cs = 0, ck0 = 0;
   auto addr = [&](int k) -> const float4* {   // k < total, k non-decreasing across calls
     for (;;) {
@@ -89,6 +90,7 @@ __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, i
     if (q1) { acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w; }
     if (q2) { acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w; }
   }
+  if (dbg && threadIdx.x == 0) dbg[6] = gtimer();
   // lane phases (lanes CB apart) by a butterfly
   for (int o = CB; o < 32; o <<= 1) {
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -98,6 +100,7 @@ __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, i
   }
   red[warp * 32 + lane] = acc;
   __syncthreads();
+  if (dbg && threadIdx.x == 0) dbg[7] = gtimer();
   if (warp == 0 && lane < CB && active) {
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
     if (residual) {

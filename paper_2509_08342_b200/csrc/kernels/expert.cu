@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     __syncthreads();
     const int nblk = combine_blocks(p.B, d);
     for (int blk = blockIdx.x; blk < nblk; blk += G)
-      combine_block(blk, cs, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red);
+      combine_block(blk, cs, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red, dbg);
   }
   __syncthreads();
   if (dbg && tid == 0) dbg[4] = gtimer();

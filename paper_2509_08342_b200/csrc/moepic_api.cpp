@@ -783,17 +783,19 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       unsigned long long h[148 * 8];
       cudaStreamSynchronize(s);
       cudaMemcpy(h, dbg_buf, sizeof h, cudaMemcpyDeviceToHost);
-      unsigned long long t0 = ~0ull, mx[5] = {0, 0, 0, 0, 0}, mn[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+      unsigned long long t0 = ~0ull, mx[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mn[8];
+      for (auto& v : mn) v = ~0ull;
       for (int c = 0; c < G; ++c) t0 = std::min(t0, h[c * 8]);
       for (int c = 0; c < G; ++c)
-        for (int k = 0; k < 5; ++k)
+        for (int k = 0; k < 8; ++k)
           if (h[c * 8 + k]) {
             mx[k] = std::max(mx[k], h[c * 8 + k] - t0);
             mn[k] = std::min(mn[k], h[c * 8 + k] - t0);
           }
       fprintf(stderr, "[k2trace] G=%lld rows=%lld comb=%d start %llu..%llu first_tile %llu..%llu stream_done %llu..%llu "
-              "barrier %llu..%llu end %llu..%llu ns\n", (long long)G, (long long)R, kp.combine, mn[0], mx[0], mn[1],
-              mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4]);
+              "barrier %llu..%llu end %llu..%llu ns | combine: walk-total %llu..%llu loads %llu..%llu reduce %llu..%llu\n",
+              (long long)G, (long long)R, kp.combine, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4],
+              mx[4], mn[5], mx[5], mn[6], mx[6], mn[7], mx[7]);
     }
     ctx->prof_end(pe, s, alg_bytes);
     CK(cudaGetLastError());
