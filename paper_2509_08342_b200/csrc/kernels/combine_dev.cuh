@@ -117,4 +117,113 @@ __device__ __forceinline__ void combine_block(int blk, const CombineSeg* segs, i
   __syncthreads();   // `red` is reused by the next block
 }
 
+// Flattened variant: the CTA first lists, per token, the float offsets of its partial vectors in
+// the same fixed order (segments in step order, chunks in CTA order) in shared memory, so the
+// lanes index their partials directly instead of walking the segment table.
+// Called by all kCombineWarps * 32 threads; tstart: B + 1 ints; offs: sum over tokens of their
+// partial counts (the host checks it fits).
+__device__ __forceinline__ void combine_build_table(const CombineSeg* segs, int nsegs, int B, int d, int* tstart,
+                                                    uint32_t* offs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // 1. partial count per token (one warp per token; lanes over segments)
+  for (int b = warp; b < B; b += kCombineWarps) {
+    int tot = 0;
+    for (int s0 = 0; s0 < nsegs; s0 += 32) {
+      const int s = s0 + lane;
+      int c = (s < nsegs && (segs[s].tok_mask >> b & 1u)) ? segs[s].nchunks : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      tot += c;
+    }
+    if (lane == 0) tstart[b + 1] = tot;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tstart[0] = 0;
+    for (int b = 0; b < B; ++b) tstart[b + 1] += tstart[b];
+  }
+  __syncthreads();
+  // 2. offsets: a segment's chunks at its exclusive prefix within the token
+  for (int b = warp; b < B; b += kCombineWarps) {
+    int base = tstart[b];
+    for (int s0 = 0; s0 < nsegs; s0 += 32) {
+      const int s = s0 + lane;
+      const bool has = s < nsegs && (segs[s].tok_mask >> b & 1u);
+      const int c = has ? segs[s].nchunks : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (has) {
+        const uint32_t m = segs[s].tok_mask;
+        const int ntok = __popc(m), t = __popc(m & ((1u << b) - 1u));
+        const int64_t o0 = segs[s].ws_off + (int64_t)t * d;
+        for (int k = 0; k < c; ++k) offs[base + incl - c + k] = (uint32_t)(o0 + (int64_t)k * ntok * d);
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void combine_block_flat(int blk, const int* tstart, const uint32_t* offs, const float* ws,
+                                                   const uint16_t* h, float* y, int B, int d, int residual,
+                                                   float4* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d4 = d >> 2;
+  const int CB = combine_cb(B, d);
+  const int P = 32 / CB;
+  const int S = kCombineWarps * P;
+  const int ncb = (d4 + CB - 1) / CB;
+  const int b = blk / ncb;
+  const int c4 = (blk - b * ncb) * CB + (lane % CB);
+  const int phase = warp * P + lane / CB;
+  const bool active = c4 < d4;
+  const uint32_t* ob = offs + tstart[b];
+  const int total = tstart[b + 1] - tstart[b];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (active) {
+    const float4* w4 = reinterpret_cast<const float4*>(ws) + c4;
+    int k = phase;
+    for (; k + 3 * S < total; k += 4 * S) {
+      const float4 v0 = w4[ob[k] >> 2], v1 = w4[ob[k + S] >> 2], v2 = w4[ob[k + 2 * S] >> 2], v3 = w4[ob[k + 3 * S] >> 2];
+      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+      acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+      acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    }
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 v0 = k < total ? w4[ob[k] >> 2] : z;
+    const float4 v1 = k + S < total ? w4[ob[k + S] >> 2] : z;
+    const float4 v2 = k + 2 * S < total ? w4[ob[k + 2 * S] >> 2] : z;
+    if (k < total) { acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w; }
+    if (k + S < total) { acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w; }
+    if (k + 2 * S < total) { acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w; }
+  }
+  for (int o = CB; o < 32; o <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  red[warp * 32 + lane] = acc;
+  __syncthreads();
+  if (warp == 0 && lane < CB && active) {
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (residual) {
+      const uint2 hv = reinterpret_cast<const uint2*>(h + (size_t)b * d)[c4];
+      r = make_float4(bf16lo(hv.x), bf16hi(hv.x), bf16lo(hv.y), bf16hi(hv.y));
+    }
+#pragma unroll
+    for (int w = 0; w < kCombineWarps; ++w) {
+      const float4 v = red[w * 32 + lane];
+      r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
+    }
+    reinterpret_cast<float4*>(y + (size_t)b * d)[c4] = r;
+  }
+  __syncthreads();
+}
+
 }  // namespace moepic

@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       unsigned long long v;
       do {
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.bar) : "memory");
-        if (v < p.bar_target) __nanosleep(100);
+        if (v < p.bar_target) __nanosleep(20);
       } while (v < p.bar_target);
       __threadfence();
     }
@@ -434,14 +434,24 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     // CTA c combines column blocks c, c + G, ... (combine_dev.cuh: 16 warps over the partials,
     // lanes over 32 float4 columns, fixed order); the K2 smem ring is free again here
     // the segment table goes to shared memory first: the combine's lanes walk it at different
-    // positions, which the constant cache behind the kernel parameters would serialise
+    // positions, which the constant cache behind the kernel parameters would serialise; with
+    // p.flat the per-token partial offsets are listed once (combine_build_table) and indexed
     float4* red = reinterpret_cast<float4*>(smem);
     CombineSeg* cs = reinterpret_cast<CombineSeg*>(smem + kConsumerWarps * 32 * sizeof(float4));
     for (int i = tid; i < p.ncomb; i += kThreads) cs[i] = p.comb[i];
     __syncthreads();
     const int nblk = combine_blocks(p.B, d);
-    for (int blk = blockIdx.x; blk < nblk; blk += G)
-      combine_block(blk, cs, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red, dbg);
+    if (p.flat) {
+      int* tstart = reinterpret_cast<int*>(cs + p.ncomb);
+      uint32_t* offs = reinterpret_cast<uint32_t*>(tstart + 36);
+      combine_build_table(cs, p.ncomb, p.B, d, tstart, offs);
+      if (dbg && tid == 0) dbg[5] = gtimer();
+      for (int blk = blockIdx.x; blk < nblk; blk += G)
+        combine_block_flat(blk, tstart, offs, p.ws, p.h, p.y, p.B, d, p.residual, red);
+    } else {
+      for (int blk = blockIdx.x; blk < nblk; blk += G)
+        combine_block(blk, cs, p.ncomb, p.ws, p.h, p.y, p.B, d, p.residual, red, dbg);
+    }
   }
   __syncthreads();
   if (dbg && tid == 0) dbg[4] = gtimer();
@@ -459,7 +469,7 @@ struct K2ParamsCap {
   int64_t total_rows;
   int d, K, nsegs;
   Seg segs[CAP];
-  int combine, B, residual, ncomb;
+  int combine, B, residual, ncomb, flat;
   float* y;
   unsigned long long* bar;
   unsigned long long bar_target;
@@ -474,7 +484,7 @@ static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   q.h = p.h; q.ids = p.ids; q.w = p.w; q.ws = p.ws; q.total_rows = p.total_rows;
   q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
-  q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0;
+  q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0; q.flat = p.flat;
   q.y = p.y; q.bar = p.bar; q.bar_target = p.bar_target; q.tstamp = p.tstamp; q.dbg = p.dbg;
   for (int i = 0; i < q.ncomb; ++i) q.comb[i] = p.comb[i];
   auto* fn = k2_split_expert<TB, CW, RS, Q4, K2ParamsCap<CAP>>;

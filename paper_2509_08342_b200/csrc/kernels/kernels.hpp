@@ -81,6 +81,7 @@ struct K2Params {
   // fused combine (the step's final K2 launch, cooperative): after a grid barrier every CTA adds
   // a slice of the step's partials in K3's fixed order
   int combine, B, residual, ncomb;
+  int flat;                         // the combine lists per-token partial offsets in shared memory
   float* y;
   unsigned long long* bar;
   unsigned long long bar_target;

@@ -763,6 +763,11 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       kp.y = fuse->y;
       kp.ncomb = (int)comb.size();
       for (size_t i = 0; i < comb.size(); ++i) kp.comb[i] = comb[i];
+      // flattened offsets fit next to the reduction area and the segment table in the K2 ring
+      uint64_t noff = 0;
+      for (const auto& c : comb) noff += (uint64_t)c.nchunks * __builtin_popcount(c.tok_mask);
+      const uint64_t need = 16ull * 32 * 16 + comb.size() * sizeof(CombineSeg) + 36 * 4 + noff * 4;
+      kp.flat = need <= (uint64_t)k2_smem_bytes(d, kp.q4) ? 1 : 0;
       kp.bar = reinterpret_cast<unsigned long long*>(ctx->arena + ctx->lay.ticket + 8);
       ctx->bar_base += (uint64_t)G;
       kp.bar_target = ctx->bar_base;
