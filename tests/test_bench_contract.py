@@ -53,3 +53,15 @@ def test_our_arm_contract_toy():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "clocks" in d
+
+
+@pytest.mark.gpu
+def test_our_arm_modes_toy():
+    """The Q4G64 and attention stand-in modes keep the contract and label themselves."""
+    d = _run(["--config", "toy", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--weights", "q4",
+              "--no-cpu-baseline"])
+    assert d["value"] > 0 and d["config"]["weights"] == "q4" and d["dtype"] != "bf16"
+    d = _run(["--config", "toy", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--attention", "300",
+              "--no-cpu-baseline"])
+    a = d["config"]["attention"]
+    assert d["value"] > 0 and a["kv_positions"] == 300 and a["us_per_layer"] > 0
