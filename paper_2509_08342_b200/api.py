@@ -187,7 +187,7 @@ class MoEpic:
     def layer_forward_host(self, layer, h_bits: np.ndarray, stream=None, flags=0, trace=True):
         a = np.ascontiguousarray(h_bits, dtype=np.uint16)
         B = a.shape[0]
-        y = np.zeros((B, self.desc.d), np.float32)
+        y = np.empty((B, self.desc.d), np.float32)   # fully written by the call
         sp = C.c_void_p(stream.cuda_stream if stream is not None else None)
         tp = C.byref(self._tb.t) if trace else None
         self._err(M.moepic_layer_forward_host(self.h, layer, _ptr(a, C.c_uint16), B, _ptr(y, C.c_float), sp,

@@ -37,7 +37,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
-  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, hstage, total;
+  size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, hstage, ystage, total;
   uint64_t pool_rows, plan_rows, od_rows, ws_floats;
   // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
   size_t xperm, aact, yperm, pos, cursor;
@@ -119,6 +119,8 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   a.rsel = off; off = align_up(off + (size_t)d.N * 16);   // k1_select: cnt int32 [N] | max u64 [N]
   a.trec = off; off = align_up(off + (size_t)2 * kProfRing * 8);   // profiling: start [ring] | end [ring]
   a.hstage = off; off = align_up(off + (size_t)d.max_batch * d.d * 2);   // layer_forward_host input rows
+  a.ystage = off;                                                          // ... and prefill outputs
+  if (d.max_batch > kDecodeMaxB) off = align_up(off + (size_t)d.max_batch * d.d * 4);
   a.pf_rows = 0;
   a.xperm = a.aact = a.yperm = a.pos = a.cursor = off;
   if (d.max_batch > kDecodeMaxB) {
@@ -1409,6 +1411,21 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   return MOEPIC_OK;
 }
 
+// host memcpy of prefill-sized buffers (tens of MB) split over the OpenMP threads
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = 1u << 20;
+  if (bytes <= 2 * kPiece) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  const long n = (long)((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static)
+  for (long i = 0; i < n; ++i) {
+    const size_t off = (size_t)i * kPiece;
+    memcpy(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off, std::min(kPiece, bytes - off));
+  }
+}
+
 moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const uint16_t* h_host, int32_t B,
                                         float* y_host, void* stream, uint32_t flags, moepic_trace* tr) {
   CTX_GUARD();
@@ -1421,15 +1438,20 @@ moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const ui
   // h: host -> mapped pinned staging -> arena (SM loads, not the busy H2D copy engine);
   // y: the combine stores straight into the mapped staging (zero-copy), read after the sync.
   // Both buffers are allocated at create, so no allocation happens on this path.
-  memcpy(ctx->scratch_h, h_host, hb);
+  par_memcpy(ctx->scratch_h, h_host, hb);
   uint8_t* ds = ctx->arena + ctx->lay.hstage;
   launch_stage_in(ds, ctx->scratch_d, (hb + 15) / 16 * 16, s);
   CK(cudaGetLastError());
-  moepic_status st = moepic_layer_forward(ctx, layer, ds, B, reinterpret_cast<float*>(ctx->scratch_d + yoff),
-                                          stream, flags, tr);
+  // prefill outputs (MBs) are written to device memory and read back by the D2H copy engine
+  // (the device->host direction is idle; scattered SM stores into host memory crawl)
+  const bool big = B > kDecodeMaxB;
+  float* yd = big ? reinterpret_cast<float*>(ctx->arena + ctx->lay.ystage)
+                  : reinterpret_cast<float*>(ctx->scratch_d + yoff);
+  moepic_status st = moepic_layer_forward(ctx, layer, ds, B, yd, stream, flags, tr);
   if (st != MOEPIC_OK) return st;
+  if (big) CK(cudaMemcpyAsync(ctx->scratch_h + yoff, yd, yb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  memcpy(y_host, ctx->scratch_h + yoff, yb);
+  par_memcpy(y_host, ctx->scratch_h + yoff, yb);
   return MOEPIC_OK;
 }
 
