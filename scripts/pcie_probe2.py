@@ -1,5 +1,6 @@
-"""H2D bandwidth of one vs several concurrent copy streams and of SM loads from mapped pinned
-memory (tools only): does splitting the transfer engine's copies raise the link rate?"""
+"""H2D bandwidth of one vs several concurrent copy streams and of 8 MB chunks on one stream
+(tools only): does splitting the transfer engine's copies raise the link rate?  SM loads from
+mapped pinned memory are probed in scripts/pcie_zero_copy.py."""
 import json
 import torch
 
