@@ -430,8 +430,17 @@ def run_ours(args, log):
     if prefill:
         tf = kg["bytes"] / (kg["total_ms"] * 1e-3) / 1e12 if kg["total_ms"] > 0 else 0.0
         tpeak = float(peaks.get("bf16_tflops_sustained", 1440.6))
+        traffic, tsrc = None, None
+        try:   # ncu --set full DRAM bytes per flop of the GEMM pair on a resident layer, same T
+            ent = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.config]
+            if kg["launches"] and "dram_bytes_per_flop" in ent:
+                traffic = int(ent["dram_bytes_per_flop"] * kg["bytes"] / kg["launches"])
+                tsrc = {k: ent[k] for k in ("dram_bytes_per_layer", "alg_bytes_per_layer", "ratio", "report")}
+        except Exception:
+            pass
         roof = {"bound": "tensor", "kernel": "pf_gemm (tcgen05 gate/up + down)", "achieved": round(tf, 1),
-                "peak": tpeak, "unit": "TFLOP/s", "frac": round(tf / tpeak, 4), "traffic": None,
+                "peak": tpeak, "unit": "TFLOP/s", "frac": round(tf / tpeak, 4), "traffic": traffic,
+                "traffic_source": tsrc,
                 "launches": kg["launches"], "avg_launch_us": round(kg["total_ms"] * 1e3 / max(1, kg["launches"]), 2),
                 "flops_per_launch": int(kg["bytes"] / max(1, kg["launches"])),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
