@@ -238,7 +238,7 @@ struct moepic_ctx {
   uint8_t* mailbox = nullptr;        // mapped pinned
   uint8_t* mailbox_dev = nullptr;
   cudaStream_t copy = nullptr;
-  cudaEvent_t ev_od = nullptr, ev_plan[2] = {nullptr, nullptr}, ev_step[2] = {nullptr, nullptr};
+  cudaEvent_t ev_od = nullptr, ev_od_head = nullptr, ev_plan[2] = {nullptr, nullptr}, ev_step[2] = {nullptr, nullptr};
   bool ev_step_rec[2] = {false, false};
   cudaEvent_t ev_tmp = nullptr;
   std::vector<uint64_t> slot_base;   // per layer: byte offset inside the pool
@@ -266,6 +266,9 @@ struct moepic_ctx {
     int32_t item;
   };
   size_t kFeedChunk = 8ull << 20;
+  // decode: the step's last on-demand copy is split so its final tail_bytes land last; the K2
+  // launch over everything else runs while the tail is still in flight (0 disables)
+  size_t od_tail_bytes = 64ull << 20;
   size_t kFeedDepth = 3;
   static constexpr int kFeedRing = 16;
   bool cancel_prefetch = true;
@@ -464,7 +467,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->mailbox_dev), ctx->mailbox, 0) != cudaSuccess)
     return bail(MOEPIC_ERUNTIME);
   if (cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
-  cudaEvent_t* evs[] = {&ctx->ev_od, &ctx->ev_plan[0], &ctx->ev_plan[1], &ctx->ev_step[0], &ctx->ev_step[1],
+  cudaEvent_t* evs[] = {&ctx->ev_od, &ctx->ev_od_head, &ctx->ev_plan[0], &ctx->ev_plan[1], &ctx->ev_step[0], &ctx->ev_step[1],
                         &ctx->ev_tmp};
   for (auto* e : evs)
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
@@ -474,6 +477,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
       cudaMemset(ctx->arena + lay.rsel, 0, (size_t)desc->N * 16) != cudaSuccess)
     return bail(MOEPIC_ERUNTIME);
   if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;
+  if (const char* e = getenv("MOEPIC_OD_TAIL_MB")) ctx->od_tail_bytes = (size_t)atol(e) << 20;
   if (const char* e = getenv("MOEPIC_FEED_DEPTH")) ctx->kFeedDepth = (size_t)std::min(atol(e), (long)moepic_ctx::kFeedRing);
   if (const char* e = getenv("MOEPIC_PF_CTA_PAIR")) ctx->pf_cta_pair = atoi(e) ? 1 : 0;
   ctx->k1_trace = getenv("MOEPIC_K1_TRACE") != nullptr;
@@ -1225,6 +1229,8 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   int64_t od_row = 0;
   int n_od = 0;
   bool waited = false;
+  struct HeldCopy { uint8_t* dst; const uint8_t* src; size_t bytes; } held{nullptr, nullptr, 0};
+  const bool split_ok = B <= kDecodeMaxB && ctx->od_tail_bytes > 0;
   auto copy = [&](uint8_t* dst, const uint8_t* src, size_t bytes) -> moepic_status {
     const auto tw0 = std::chrono::steady_clock::now();
     if (!waited) {   // the buffers / slots written here were last read by earlier steps
@@ -1233,13 +1239,22 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       waited = true;
     }
     const auto tw1 = std::chrono::steady_clock::now();
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
+    if (held.bytes) {   // a later copy exists: the held one is not the step's last, issue it whole
+      CK(cudaMemcpyAsync(held.dst, held.src, held.bytes, cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies++;
+      held.bytes = 0;
+    }
+    if (split_ok && bytes > 2 * ctx->od_tail_bytes) {
+      held = HeldCopy{dst, src, bytes};   // may be the last: issued (maybe split) by the next call or at the end
+    } else {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies++;
+    }
     if (ctx->host_timing) {
       ctx->hc[0] += std::chrono::duration<double, std::micro>(tw1 - tw0).count();
       ctx->hc[1] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw1).count();
       ctx->hc_n++;
     }
-    ctx->ctr.h2d_copies++;
     if (n_od++ == 0 && ctx->host_timing) t_first_copy = std::chrono::steady_clock::now();
     return MOEPIC_OK;
   };
@@ -1298,6 +1313,28 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     if ((st = copy(top, ctx->host_expert(layer, e), (size_t)l.I_top * rb)) != MOEPIC_OK) return st;
     gC.push_back(StepSeg{top, e, l.I_top, masks[a], 0});
   }
+  // the step's last on-demand copy, if held: head, an event, then the tail (gC's last entry)
+  const uint8_t* tail_base = nullptr;
+  if (held.bytes) {
+    const int64_t tail_rows = (int64_t)((ctx->od_tail_bytes + rb - 1) / rb);
+    StepSeg& last = gC.back();
+    const size_t head_bytes = (size_t)(last.nrows - tail_rows) * rb;
+    if (last.base != held.dst || (size_t)last.nrows * rb != held.bytes || tail_rows >= last.nrows)
+      return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: held copy does not match the last on-demand segment");
+    CK(cudaMemcpyAsync(held.dst, held.src, head_bytes, cudaMemcpyHostToDevice, ctx->copy));
+    CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
+    CK(cudaMemcpyAsync(held.dst + head_bytes, held.src + head_bytes, held.bytes - head_bytes,
+                       cudaMemcpyHostToDevice, ctx->copy));
+    ctx->ctr.h2d_copies += 2;
+    StepSeg tail = last;
+    last.nrows -= (int32_t)tail_rows;
+    tail.base = held.dst + head_bytes;
+    tail.nrows = (int32_t)tail_rows;
+    tail.row0 = last.row0 + last.nrows;
+    gC.push_back(tail);
+    tail_base = tail.base;
+    held.bytes = 0;
+  }
   if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
   {   // an expert's on-demand segments consecutive, tops first (the prefill down GEMM groups by expert)
     std::vector<int32_t> pos(d.N, 0);
@@ -1306,6 +1343,8 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       const int px = x.expert >= 0 ? pos[x.expert] : -1, py = y.expert >= 0 ? pos[y.expert] : -1;
       return px != py ? px < py : x.row0 < y.row0;
     });
+    if (tail_base)   // the split tail lands last: it goes last (its own K2 launch)
+      std::stable_partition(gC.begin(), gC.end(), [&](const StepSeg& x) { return x.base != tail_base; });
   }
   const auto t_copies = std::chrono::steady_clock::now();
 
@@ -1318,6 +1357,22 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   int64_t ws_next = 0;
   std::vector<CombineSeg> comb;
   FuseCombine fuse{y_dev, adds_residual(d, flags) ? 1 : 0, false};
+  if (tail_base) {
+    // split last copy: ONE launch over the resident, prefetched and on-demand rows except the
+    // tail once the head has landed (it runs while the tail is in flight), then the tail with
+    // the fused combine -- the link idles only for the tail's K2, not for the whole on-demand set
+    std::vector<StepSeg> first(gA);
+    first.insert(first.end(), gB.begin(), gB.end());
+    first.insert(first.end(), gC.begin(), gC.end() - 1);
+    std::vector<StepSeg> tail(gC.end() - 1, gC.end());
+    if (!gB.empty()) CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
+    CK(cudaStreamWaitEvent(s, ctx->ev_od_head, 0));
+    st = launch_group(ctx, first, h, B, s, ws_next, comb, launches, nullptr);
+    if (st != MOEPIC_OK) return st;
+    CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
+    st = launch_group(ctx, tail, h, B, s, ws_next, comb, launches, &fuse);
+    if (st != MOEPIC_OK) return st;
+  } else {
   const bool lastA = gB.empty() && gC.empty(), lastB = gC.empty();
   st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches, lastA ? &fuse : nullptr);
   if (st != MOEPIC_OK) return st;
@@ -1330,6 +1385,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
     st = launch_group(ctx, gC, h, B, s, ws_next, comb, launches, &fuse);
     if (st != MOEPIC_OK) return st;
+  }
   }
   if (!fuse.done) {   // no K2 launch fused the combine (no segments, or too many): run K3
   if (comb.size() > (size_t)kMaxStepSegs) return fail(&ctx->err, MOEPIC_ERUNTIME, "too many segments in one step");
@@ -1640,7 +1696,7 @@ void moepic_destroy(moepic_ctx* ctx) {
     cudaEventDestroy(pe.a);
     cudaEventDestroy(pe.b);
   }
-  cudaEvent_t evs[] = {ctx->ev_od, ctx->ev_plan[0], ctx->ev_plan[1], ctx->ev_step[0], ctx->ev_step[1], ctx->ev_tmp};
+  cudaEvent_t evs[] = {ctx->ev_od, ctx->ev_od_head, ctx->ev_plan[0], ctx->ev_plan[1], ctx->ev_step[0], ctx->ev_step[1], ctx->ev_tmp};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   if (ctx->host_experts) cudaFreeHost(ctx->host_experts);
