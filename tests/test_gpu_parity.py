@@ -183,6 +183,36 @@ def test_qwen3_shape(B):
     _replay(m, ctx, orc, toks, api.M.FUSE_PREDICT)
 
 
+@pytest.mark.parametrize("B,tail_kb", [(1, 256), (4, 256), (16, 1024), (4, 4000)])
+def test_od_tail_split(B, tail_kb, monkeypatch):
+    """The layer's last on-demand copy split into head + tail (MOEPIC_OD_TAIL_KB, read at create):
+    one K2 launch over the resident, prefetched and head rows, then the tail with the fused
+    combine.  Qwen3 shape, where bottoms are 4.7 MB: 256 KB / 1 MB tails split every layer; a
+    4000 KB tail is over half a bottom, so nothing is split.  Same traces, y within TOL."""
+    api = _api()
+    S = synth.SHAPES["qwen3"]
+    m = Model(2, S.N, S.K, S.d, S.I, seed=3, gen_device="cuda")
+    H = synth.hidden_states(6, 3 * B, 2, S.d)
+    toks = [[H[t * B:(t + 1) * B, i] for i in range(2)] for t in range(3)]
+    copies = {}
+    for kb in (tail_kb, 0):      # 0: no split (the reference count of copies)
+        monkeypatch.setenv("MOEPIC_OD_TAIL_KB", str(kb))
+        ctx = _ctx(m, max_batch=B, v_e_max=128.0)
+        orc = OracleEngine(2, S.N, S.K, S.d, S.I)
+        cfg = dict(v_e=128.0, seed=5)
+        ctx.configure(**cfg)
+        orc.configure(CacheConfig(**cfg))
+        c0 = ctx.counters()
+        _replay(m, ctx, orc, toks, api.M.FUSE_PREDICT)
+        copies[kb] = ctx.counters()["h2d_copies"] - c0["h2d_copies"]
+        del ctx
+    extra = copies[tail_kb] - copies[0]      # one extra copy per split layer step (6 steps)
+    if tail_kb < 2000:
+        assert 0 < extra <= 6, copies
+    else:
+        assert extra == 0, copies
+
+
 def test_deepseek_shape_shared_no_renorm():
     """BJ config 3 shape: 64 routed + 2 shared experts top-6, d 2048, I 1408, renorm off (Q4)."""
     api = _api()
