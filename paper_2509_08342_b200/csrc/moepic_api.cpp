@@ -1281,7 +1281,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       // rows follow in pass 2, once admission has chosen their destination)
       const int rows = d.I - l.I_top;
       uint8_t* dst = ctx->od_ptr(buf, od_row);
-      if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+      if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
       if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)l.I_top * rb, (size_t)rows * rb)) != MOEPIC_OK) return st;
       gC.push_back(StepSeg{dst, e, rows, m, l.I_top});
       od_row += rows;
@@ -1307,7 +1307,7 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     if (slot >= 0) {
       top = ctx->slot_ptr(layer, slot);
     } else {
-      if ((uint64_t)(od_row + l.I_top) > ctx->lay.od_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+      if ((uint64_t)(od_row + l.I_top) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
       top = ctx->od_ptr(buf, od_row);
       od_row += l.I_top;
     }
@@ -1321,7 +1321,8 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     StepSeg& last = gC.back();
     const size_t head_bytes = (size_t)(last.nrows - tail_rows) * rb;
     if (last.base != held.dst || (size_t)last.nrows * rb != held.bytes || tail_rows >= last.nrows)
-      return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: held copy does not match the last on-demand segment");
+      return ctx->poisoned = true,
+             fail(&ctx->err, MOEPIC_ERUNTIME, "internal: held copy does not match the last on-demand segment");
     CK(cudaMemcpyAsync(held.dst, held.src, head_bytes, cudaMemcpyHostToDevice, ctx->copy));
     CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
     CK(cudaMemcpyAsync(held.dst + head_bytes, held.src + head_bytes, held.bytes - head_bytes,
