@@ -398,6 +398,7 @@ def run_ours(args, log):
             yp = torch.empty(B, S.d, dtype=torch.float32).pin_memory()
             hd = torch.empty(B, S.d, dtype=torch.int16, device="cuda")
             dist.barrier()
+        ce0 = ctx.counters()
         e0.record(stream)
         for t in range(args.e2e_steps):
             for i in range(L):
@@ -419,6 +420,13 @@ def run_ours(args, log):
         e2e = {"value": round(args.e2e_steps * B / (ems / 1e3), 4), "unit": "tokens/s",
                "h2d_bytes_per_step": L * B * S.d * 2, "d2h_bytes_per_step": L * B * S.d * 4,
                "api": "moepic_layer_forward + all_reduce (pinned staging)" if dist else "moepic_layer_forward_host"}
+        # the e2e tokens are later tokens of the same process: their own PCIe bytes and path
+        # fraction separate the API's per-layer round trip from a different byte mix
+        ce1 = ctx.counters()
+        e2e_pcie = (ce1["pcie_ondemand_bytes"] - ce0["pcie_ondemand_bytes"] +
+                    ce1["pcie_prefetch_bytes"] - ce0["pcie_prefetch_bytes"])
+        e2e["pcie_bytes_moved"] = int(e2e_pcie)
+        e2e["path_frac"] = round(e2e_pcie / (pcie * 1e9) / (ems / 1e3), 4) if ems > 0 else None
 
     peaks = _peaks()
     hbm_peak = float(peaks["hbm_gbs"])

@@ -315,6 +315,8 @@ struct moepic_ctx {
   double hp[4] = {0, 0, 0, 0};
   double hf[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t hf_n = 0;
+  double hh[3] = {0, 0, 0};   // host-buffer entry: stage-in, forward call, sync + y read (us)
+  uint64_t hh_n = 0;
   uint64_t hc_n = 0;
   uint64_t ht_n = 0;
   unsigned long long* k1dbg = nullptr;   // MOEPIC_K1_TRACE ring (tools)
@@ -1496,6 +1498,7 @@ moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const ui
   // h: host -> mapped pinned staging -> arena (SM loads, not the busy H2D copy engine);
   // y: the combine stores straight into the mapped staging (zero-copy), read after the sync.
   // Both buffers are allocated at create, so no allocation happens on this path.
+  const auto th0 = std::chrono::steady_clock::now();
   par_memcpy(ctx->scratch_h, h_host, hb);
   uint8_t* ds = ctx->arena + ctx->lay.hstage;
   launch_stage_in(ds, ctx->scratch_d, (hb + 15) / 16 * 16, s);
@@ -1505,11 +1508,21 @@ moepic_status moepic_layer_forward_host(moepic_ctx* ctx, int32_t layer, const ui
   const bool big = B > kDecodeMaxB;
   float* yd = big ? reinterpret_cast<float*>(ctx->arena + ctx->lay.ystage)
                   : reinterpret_cast<float*>(ctx->scratch_d + yoff);
+  const auto th1 = std::chrono::steady_clock::now();
   moepic_status st = moepic_layer_forward(ctx, layer, ds, B, yd, stream, flags, tr);
   if (st != MOEPIC_OK) return st;
+  const auto th2 = std::chrono::steady_clock::now();
   if (big) CK(cudaMemcpyAsync(ctx->scratch_h + yoff, yd, yb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   par_memcpy(y_host, ctx->scratch_h + yoff, yb);
+  if (ctx->host_timing) {   // MOEPIC_HOST_TIMING (tools)
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    const auto th3 = std::chrono::steady_clock::now();
+    ctx->hh[0] += us(th0, th1);
+    ctx->hh[1] += us(th1, th2);
+    ctx->hh[2] += us(th2, th3);
+    ctx->hh_n++;
+  }
   return MOEPIC_OK;
 }
 
@@ -1661,6 +1674,9 @@ void moepic_destroy(moepic_ctx* ctx) {
     fprintf(stderr, "[hosttiming] %llu calls: launch router + wait routing %.1f | routing -> first copy issued %.1f | "
             "routing -> all copies issued %.1f | K2 launches + next plan %.1f us\n", (unsigned long long)ctx->ht_n,
             ctx->ht[0] / ctx->ht_n, ctx->ht[1] / ctx->ht_n, ctx->ht[2] / ctx->ht_n, ctx->ht[3] / ctx->ht_n);
+  if (ctx->hh_n)
+    fprintf(stderr, "[hosttiming] host-buffer entry x%llu: stage-in %.1f, forward call %.1f, sync + y read %.1f us\n",
+            (unsigned long long)ctx->hh_n, ctx->hh[0] / ctx->hh_n, ctx->hh[1] / ctx->hh_n, ctx->hh[2] / ctx->hh_n);
   if (ctx->ht_n)
     fprintf(stderr, "[hosttiming] classify %.1f, finish_plan %.1f, pass 1 %.1f, commit %.1f us\n", ctx->hp[0] / ctx->ht_n,
             ctx->hp[1] / ctx->ht_n, ctx->hp[2] / ctx->ht_n, ctx->hp[3] / ctx->ht_n);
