@@ -73,6 +73,108 @@ def test_stats_invariants_and_bruteforce_recount():
         assert st.H(C) == hits[C] / (80 * K)
 
 
+def test_stats_P_PH_hand_worked_example():
+    """P(y) and PH(y, C) on a 3-token trace, every value derived by hand.
+
+    N = 4, K = 1.  The size-C cache is the top-C by pre-step activation count, ties by
+    smaller id (reading Q15).  Token by token:
+      t0: counts (0,0,0,0) -> cache order [0,1,2,3]; ids {2}; ranking R' = [2,0,1,3]
+      t1: counts (0,0,1,0) -> cache order [2,0,1,3]; ids {2}; R' = [3,2,0,1]
+      t2: counts (0,0,2,0) -> cache order [2,0,1,3]; ids {1}; R' = [1,3,2,0]
+    P(y)  = #tokens where the y-th predicted expert is activated / q:
+      y=1: t0 (2 in {2}) yes, t1 (3) no, t2 (1) yes -> 2/3
+      y=2: t0 (0) no, t1 (2) yes, t2 (3) no          -> 1/3
+      y=3, y=4: never                                 -> 0
+    PH(y, C) = #tokens where the y-th predicted expert is in the size-C cache / q:
+      y=1: t0 expert 2 has cache position 3; t1 expert 3 has 4; t2 expert 1 has 3
+           -> PH(1,1)=PH(1,2)=0, PH(1,3)=2/3, PH(1,4)=1
+      y=2: t0 expert 0 position 1; t1 expert 2 position 1; t2 expert 3 position 4
+           -> PH(2,1)=PH(2,2)=PH(2,3)=2/3, PH(2,4)=1
+    A mutation that ranks the y-th position itself (rank[y] instead of rank[R'[y]]) or
+    counts the activated expert instead of the predicted one fails here."""
+    st = LayerStats(4, 1)
+    st.observe(np.array([[2]]), np.array([2, 0, 1, 3]))
+    st.observe(np.array([[2]]), np.array([3, 2, 0, 1]))
+    st.observe(np.array([[1]]), np.array([1, 3, 2, 0]))
+    assert [st.P(y) for y in (1, 2, 3, 4)] == [2 / 3, 1 / 3, 0.0, 0.0]
+    assert [st.PH(1, C) for C in (1, 2, 3, 4)] == [0.0, 0.0, 2 / 3, 1.0]
+    assert [st.PH(2, C) for C in (1, 2, 3, 4)] == [2 / 3, 2 / 3, 2 / 3, 1.0]
+    # y=3: t0 expert 1 pos 2; t1 expert 0 pos 2; t2 expert 2 pos 1
+    assert [st.PH(3, C) for C in (1, 2, 3, 4)] == [1 / 3, 1.0, 1.0, 1.0]
+    # y=4: t0 expert 3 pos 4; t1 expert 1 pos 3; t2 expert 0 pos 2
+    assert [st.PH(4, C) for C in (1, 2, 3, 4)] == [0.0, 1 / 3, 2 / 3, 1.0]
+
+
+def test_stats_P_perfect_predictor():
+    """A perfect predictor (R' lists the K activated experts first) gives P(y) = 1 for
+    y <= K and 0 beyond (P:446 with a predictor that always ranks the activated set on top;
+    the S:404 worked case uses the same P)."""
+    rng = np.random.default_rng(9)
+    N, K = 12, 3
+    st = LayerStats(N, K)
+    for _ in range(50):
+        ids = rng.choice(N, size=K, replace=False)
+        rest = [e for e in rng.permutation(N) if e not in set(ids)]
+        st.observe(ids[None], np.array(list(rng.permutation(ids)) + rest))
+    assert [st.P(y) for y in range(1, N + 1)] == [1.0] * K + [0.0] * (N - K)
+    # an anti-predictor (activated experts ranked last) -> P(y) = 1 exactly for y > N - K
+    st = LayerStats(N, K)
+    for _ in range(50):
+        ids = rng.choice(N, size=K, replace=False)
+        rest = [e for e in rng.permutation(N) if e not in set(ids)]
+        st.observe(ids[None], np.array(rest + list(ids)))
+    assert [st.P(y) for y in range(1, N + 1)] == [0.0] * (N - K) + [1.0] * K
+
+
+def test_stats_P_PH_bruteforce_recount_batched():
+    """Brute-force recount of P(y) and PH(y, C) for every y and C from the raw
+    (ids, ranking) trace, written from the definitions P:446-447 in a different form than
+    the oracle (membership tests against an explicitly sorted cache list, not rank
+    histograms), with B > 1 token batches (reading Q9/Q15: one cache state per step,
+    every token counts), plus steps without a prediction (excluded from q_pred).
+    Also PH monotone non-decreasing in C, PH(y, N) = 1 and sum_y PH(y, C) = C."""
+    rng = np.random.default_rng(21)
+    N, K = 9, 2
+    st = LayerStats(N, K)
+    trace = []
+    for t in range(60):
+        B = int(rng.integers(1, 4))
+        ids = np.stack([rng.choice(N, size=K, replace=False, p=np.arange(1, N + 1) / (N * (N + 1) / 2))
+                        for _ in range(B)])
+        ranking = None if t % 7 == 3 else rng.permutation(N)
+        st.observe(ids, ranking)
+        trace.append((ids, ranking))
+    freq = [0] * N
+    q_pred = 0
+    p_cnt = [0] * (N + 1)
+    ph_cnt = [[0] * (N + 1) for _ in range(N + 1)]
+    for ids, ranking in trace:
+        cache_order = sorted(range(N), key=lambda e: (-freq[e], e))
+        if ranking is not None:
+            for row in ids:
+                q_pred += 1
+                for y in range(1, N + 1):
+                    pred = int(ranking[y - 1])
+                    if pred in [int(x) for x in row]:
+                        p_cnt[y] += 1
+                    for C in range(1, N + 1):
+                        if pred in cache_order[:C]:
+                            ph_cnt[y][C] += 1
+        for row in ids:
+            for e in row:
+                freq[int(e)] += 1
+    assert st.q_pred == q_pred
+    for y in range(1, N + 1):
+        assert st.P(y) == p_cnt[y] / q_pred
+        for C in range(1, N + 1):
+            assert st.PH(y, C) == ph_cnt[y][C] / q_pred
+        PHs = [st.PH(y, C) for C in range(1, N + 1)]
+        assert all(a <= b for a, b in zip(PHs, PHs[1:])) and PHs[-1] == 1.0
+    # every token's ranking is a permutation: exactly C of its N predicted experts are cached
+    for C in range(1, N + 1):
+        assert abs(sum(st.PH(y, C) for y in range(1, N + 1)) - C) < 1e-12
+
+
 # ----------------------------------------------------------------- configurator
 class FakeStats:
     """Stats with prescribed H / P / PH (for worked sub-problem cases)."""
