@@ -42,6 +42,12 @@ moepic_status moepic_hostsim_predict(moepic_hostsim* hs, int32_t next_layer, con
 /* cached set of a layer: writes up to N expert ids (ascending) into out, count into *n. */
 moepic_status moepic_hostsim_cached(moepic_hostsim* hs, int32_t layer, int32_t* out, int32_t* n);
 
+/* as moepic_get_stats / moepic_set_stats (same snapshot format, interchangeable with a
+ * context of the same (L, N, K)): statistics H/P/PH accumulators and the cache
+ * counters mu / nu / last (Eq. 4).                                                  */
+moepic_status moepic_hostsim_get_stats(moepic_hostsim* hs, void* buf, size_t* bytes);
+moepic_status moepic_hostsim_set_stats(moepic_hostsim* hs, const void* buf, size_t bytes);
+
 const char* moepic_hostsim_last_error(const moepic_hostsim* hs);
 void moepic_hostsim_destroy(moepic_hostsim* hs);
 

@@ -109,6 +109,8 @@ _sig = {
     "moepic_hostsim_predict": (C.c_int, [_ctxp, C.c_int32, _i32p, C.POINTER(moepic_trace)]),
     "moepic_hostsim_cached": (C.c_int, [_ctxp, C.c_int32, _i32p, _i32p]),
     "moepic_hostsim_last_error": (C.c_char_p, [_ctxp]),
+    "moepic_hostsim_get_stats": (C.c_int, [_ctxp, C.c_void_p, C.POINTER(C.c_size_t)]),
+    "moepic_hostsim_set_stats": (C.c_int, [_ctxp, C.c_void_p, C.c_size_t]),
     "moepic_hostsim_destroy": (None, [_ctxp]),
 }
 

@@ -267,6 +267,17 @@ class HostSim:
                   "moepic_hostsim_predict")
         return self._tb.result(0, self.desc.K)
 
+    def get_stats(self) -> bytes:
+        n = C.c_size_t()
+        self._err(M.moepic_hostsim_get_stats(self.h, None, C.byref(n)), "moepic_hostsim_get_stats")
+        buf = C.create_string_buffer(n.value)
+        self._err(M.moepic_hostsim_get_stats(self.h, buf, C.byref(n)), "moepic_hostsim_get_stats")
+        return buf.raw
+
+    def set_stats(self, blob: bytes):
+        buf = C.create_string_buffer(blob, len(blob))
+        self._err(M.moepic_hostsim_set_stats(self.h, buf, len(blob)), "moepic_hostsim_set_stats")
+
     def cached(self, layer):
         out = np.zeros(self.desc.N, np.int32)
         n = C.c_int32()

@@ -25,14 +25,38 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu", "kernels/prefill.cu",
               "kernels/attention.cu"]
 CXX_SOURCES = ["host/control.cpp", "moepic_api.cpp"]
-HEADERS = ["kernels/kernels.hpp", "kernels/device_utils.cuh", "kernels/prefill.hpp", "host/control.hpp", "../../include/moepic.h", "../../include/moepic_hostsim.h"]
+
+
+def _depfile_deps(dep):
+    """Prerequisites listed in a make-style depfile written by -MD/-MMD (None if absent)."""
+    try:
+        txt = open(dep).read()
+    except OSError:
+        return None
+    txt = txt.replace("\\\n", " ")
+    _, _, rest = txt.partition(":")
+    return [x for x in rest.split() if x and x != "\\"]
 
 
 def _newer(target, deps):
     if not os.path.exists(target):
         return True
     t = os.path.getmtime(target)
-    return any(os.path.getmtime(x) > t for x in deps)
+    return any((not os.path.exists(x)) or os.path.getmtime(x) > t for x in deps)
+
+
+def _stale(obj, src):
+    """Rebuild when the object is missing, has no depfile, or any source / header it included
+    (as the compiler itself recorded them) is newer."""
+    deps = _depfile_deps(obj + ".d")
+    return deps is None or _newer(obj, [src] + deps)
+
+
+def build_id(path=None):
+    """sha256 (16 hex) of the built library: the bench line records which binary it timed."""
+    import hashlib
+    with open(path or LIB, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
 
 
 def _run(cmd, verbose):
@@ -48,22 +72,22 @@ def _run(cmd, verbose):
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, os.path.basename(src) + ".o")
-        if force or _newer(o, [s] + hdrs):
+        if force or _stale(o, s):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-Xptxas", "-v", "--resource-usage", "-c", s, "-o", o], verbose)
+                  "-Xptxas", "-v", "--resource-usage", "-MD", "-MF", o + ".d", "-c", s, "-o", o], verbose)
         objs.append(o)
     cxx = shutil.which("g++") or "g++"
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, os.path.basename(src) + ".o")
-        if force or _newer(o, [s] + hdrs):
+        if force or _stale(o, s):
             _run([cxx, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
-                  "-Wall", "-Wno-unused-function", f"-I{CUDA}/include", "-c", s, "-o", o], verbose)
+                  "-Wall", "-Wno-unused-function", f"-I{CUDA}/include", "-MMD", "-MF", o + ".d", "-c", s, "-o", o],
+                 verbose)
         objs.append(o)
     if force or _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs,

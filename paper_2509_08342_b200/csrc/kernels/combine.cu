@@ -55,6 +55,10 @@ void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream
   k0_stage_in<<<grid, 256, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src_mapped), n16);
 }
 
+__global__ void k0_trap() { __trap(); }
+
+void launch_trap(cudaStream_t s) { k0_trap<<<1, 1, 0, s>>>(); }
+
 cudaError_t combine_init() {
   cudaError_t e = cudaSuccess, r;
   if ((r = cudaFuncSetAttribute(k3_combine<CombineParamsCap<16>>, cudaFuncAttributePreferredSharedMemoryCarveout,

@@ -111,6 +111,8 @@ void launch_combine(const CombineParams& p, cudaStream_t s);
 // host memory into device memory with SM loads, so the few KB do not queue behind the transfer
 // engine's multi-MB chunks on the host->device copy engine.  bytes % 16 == 0.
 void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
+// MOEPIC_FAULT_AT_STEP (tests): a one-thread kernel that executes a trap instruction
+void launch_trap(cudaStream_t s);
 
 // Attention stand-in (attention.cu): GQA decode over a KV cache [B][S_max][Hkv][dh], dh = 128.
 constexpr int kAttnChunk = 128;   // cache positions per split: one CTA (4 warps x 32) per split and kv head

@@ -248,6 +248,15 @@ struct moepic_ctx {
   uint32_t seq = 0;
   uint64_t bar_base = 0;             // grid-barrier arrivals so far (fused combine)
   bool poisoned = false;
+  bool committed = false;            // layer_forward: the control plane committed this step
+  // MOEPIC_FAULT_AT_STEP=n (tests): the n-th layer_forward launches a kernel that traps, so a
+  // real CUDA failure travels the ERUNTIME -> ESTATE path
+  int64_t fault_at_step = 0, fault_steps = 0;
+  // MOEPIC_POISON=1 (tests): every ping-pong half and the K2 workspace are filled
+  // with 0xFF bytes (bf16 / fp32 NaN) once the step that used them is done, the slot pool before
+  // every re-layout, and a victim's slot before the new top lands in it -- a kernel that reads a
+  // segment before its copy landed, or a stale buffer, produces NaN and fails parity
+  bool poison = false;
   std::string err;
   moepic_counters ctr{};
   // event profiling (moepic_profile): pairs recorded on the launching stream
@@ -486,6 +495,8 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   ctx->k1_trace = getenv("MOEPIC_K1_TRACE") != nullptr;
   ctx->k2_trace = getenv("MOEPIC_K2_TRACE") != nullptr;
   ctx->host_timing = getenv("MOEPIC_HOST_TIMING") != nullptr;
+  if (const char* e = getenv("MOEPIC_FAULT_AT_STEP")) ctx->fault_at_step = atol(e);
+  ctx->poison = getenv("MOEPIC_POISON") != nullptr && atoi(getenv("MOEPIC_POISON")) != 0;
   ctx->cp->solver_y_cap = getenv("MOEPIC_NO_SOLVER_YCAP") == nullptr;
   ctx->slot_base.assign(desc->L, 0);
   ctx->ids_h.resize((size_t)desc->max_batch * desc->K);
@@ -649,6 +660,7 @@ moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg, 
   std::string e = ctx->cp->configure(to_params(cfg, ctx->desc.L), ctx->lay.pool_rows);
   if (!e.empty()) return fail(&ctx->err, MOEPIC_EINVAL, "%s", e.c_str());
   // re-layout: per-layer slot regions, tops of cached experts H2D
+  if (ctx->poison) CK(cudaMemset(ctx->arena + ctx->lay.pool, 0xFF, ctx->lay.pool_rows * ctx->rb()));
   uint64_t off = 0;
   const uint64_t rb = ctx->rb();
   for (int i = 0; i < ctx->desc.L; ++i) {
@@ -864,6 +876,14 @@ static moepic_status wait_mailbox(moepic_ctx* ctx, cudaStream_t s, size_t w0, si
 }
 
 static moepic_status read_ranking(moepic_ctx* ctx, cudaStream_t s);
+
+// MOEPIC_FAULT_AT_STEP: a trapping kernel on the caller's stream, then the stream is synchronised
+// so the sticky launch failure surfaces here as it would from any real kernel fault
+static moepic_status inject_fault(moepic_ctx* ctx, cudaStream_t s) {
+  launch_trap(s);
+  CK(cudaStreamSynchronize(s));
+  return fail(&ctx->err, MOEPIC_ERUNTIME, "injected fault did not fail");
+}
 
 static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int layer_route, int layer_pred,
                                 cudaStream_t s, bool read_ids, bool read_rank) {
@@ -1168,9 +1188,8 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   return MOEPIC_OK;
 }
 
-moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B, float* y_dev,
-                                   void* stream, uint32_t flags, moepic_trace* tr) {
-  CTX_GUARD();
+static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B, float* y_dev,
+                                        void* stream, uint32_t flags, moepic_trace* tr) {
   const auto& d = ctx->desc;
   if (!ctx->configured) return fail(&ctx->err, MOEPIC_EINVAL, "moepic_configure has not been called");
   if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
@@ -1232,9 +1251,16 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   int64_t od_row = 0;
   int n_od = 0;
   bool waited = false;
-  struct HeldCopy { uint8_t* dst; const uint8_t* src; size_t bytes; } held{nullptr, nullptr, 0};
+  // The step's last on-demand copy is split (decode): every copy of more than
+  // tail_rows + 1 rows is issued at once except its final tail_rows rows, which are held; a later
+  // copy releases the held tail first.  At the end the held tail (if any) is the step's last
+  // copy: ev_od_head marks "everything but that tail landed" and the K2 launch over the rest
+  // runs while the tail is in flight.
+  struct HeldTail { uint8_t* dst; const uint8_t* src; size_t bytes; int32_t rows; } held{nullptr, nullptr, 0, 0};
   const bool split_ok = B <= kDecodeMaxB && ctx->od_tail_bytes > 0;
-  auto copy = [&](uint8_t* dst, const uint8_t* src, size_t bytes) -> moepic_status {
+  const int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
+  auto copy = [&](uint8_t* dst, const uint8_t* src, int32_t rows, bool evicted = false) -> moepic_status {
+    const size_t bytes = (size_t)rows * rb;
     const auto tw0 = std::chrono::steady_clock::now();
     if (!waited) {   // the buffers / slots written here were last read by earlier steps
       for (int b2 = 0; b2 < 2; ++b2)
@@ -1242,13 +1268,17 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       waited = true;
     }
     const auto tw1 = std::chrono::steady_clock::now();
-    if (held.bytes) {   // a later copy exists: the held one is not the step's last, issue it whole
+    if (evicted && ctx->poison) CK(cudaMemsetAsync(dst, 0xFF, bytes, ctx->copy));   // the victim's old top
+    if (held.bytes) {   // a later copy exists: the held tail is not the step's last
       CK(cudaMemcpyAsync(held.dst, held.src, held.bytes, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies++;
-      held.bytes = 0;
+      held = HeldTail{nullptr, nullptr, 0, 0};
     }
-    if (split_ok && bytes > 2 * ctx->od_tail_bytes) {
-      held = HeldCopy{dst, src, bytes};   // may be the last: issued (maybe split) by the next call or at the end
+    if (split_ok && (int64_t)rows > 2 * tail_rows_split) {
+      const size_t head = bytes - (size_t)tail_rows_split * rb;
+      CK(cudaMemcpyAsync(dst, src, head, cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies++;
+      held = HeldTail{dst + head, src + head, bytes - head, (int32_t)tail_rows_split};
     } else {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies++;
@@ -1284,13 +1314,14 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       const int rows = d.I - l.I_top;
       uint8_t* dst = ctx->od_ptr(buf, od_row);
       if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
-      if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)l.I_top * rb, (size_t)rows * rb)) != MOEPIC_OK) return st;
+      if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)l.I_top * rb, rows)) != MOEPIC_OK) return st;
       gC.push_back(StepSeg{dst, e, rows, m, l.I_top});
       od_row += rows;
     }
   }
   const auto t_p1 = std::chrono::steady_clock::now();
   cp.commit(layer, ctx->ids_h.data(), B, up, res);
+  ctx->committed = true;   // from here on, any failure leaves slots admitted with no landed rows
   const auto t_com = std::chrono::steady_clock::now();
   if (ctx->host_timing) {
     auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -1313,31 +1344,25 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
       top = ctx->od_ptr(buf, od_row);
       od_row += l.I_top;
     }
-    if ((st = copy(top, ctx->host_expert(layer, e), (size_t)l.I_top * rb)) != MOEPIC_OK) return st;
+    if ((st = copy(top, ctx->host_expert(layer, e), l.I_top, slot >= 0)) != MOEPIC_OK) return st;
     gC.push_back(StepSeg{top, e, l.I_top, masks[a], 0});
   }
-  // the step's last on-demand copy, if held: head, an event, then the tail (gC's last entry)
+  // the step's last on-demand copy, if its tail is held: an event, then the tail (gC's last entry
+  // is the segment the held tail belongs to: copy() runs right before each gC push)
   const uint8_t* tail_base = nullptr;
   if (held.bytes) {
-    const int64_t tail_rows = (int64_t)((ctx->od_tail_bytes + rb - 1) / rb);
     StepSeg& last = gC.back();
-    const size_t head_bytes = (size_t)(last.nrows - tail_rows) * rb;
-    if (last.base != held.dst || (size_t)last.nrows * rb != held.bytes || tail_rows >= last.nrows)
-      return ctx->poisoned = true,
-             fail(&ctx->err, MOEPIC_ERUNTIME, "internal: held copy does not match the last on-demand segment");
-    CK(cudaMemcpyAsync(held.dst, held.src, head_bytes, cudaMemcpyHostToDevice, ctx->copy));
     CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
-    CK(cudaMemcpyAsync(held.dst + head_bytes, held.src + head_bytes, held.bytes - head_bytes,
-                       cudaMemcpyHostToDevice, ctx->copy));
-    ctx->ctr.h2d_copies += 2;
+    CK(cudaMemcpyAsync(held.dst, held.src, held.bytes, cudaMemcpyHostToDevice, ctx->copy));
+    ctx->ctr.h2d_copies++;
     StepSeg tail = last;
-    last.nrows -= (int32_t)tail_rows;
-    tail.base = held.dst + head_bytes;
-    tail.nrows = (int32_t)tail_rows;
+    last.nrows -= held.rows;
+    tail.base = held.dst;
+    tail.nrows = held.rows;
     tail.row0 = last.row0 + last.nrows;
     gC.push_back(tail);
     tail_base = tail.base;
-    held.bytes = 0;
+    held = HeldTail{nullptr, nullptr, 0, 0};
   }
   if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
   {   // an expert's on-demand segments consecutive, tops first (the prefill down GEMM groups by expert)
@@ -1422,6 +1447,10 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
     CK(cudaMemcpyAsync(ctx->slot_ptr(layer, a.slot), ctx->plan_ptr(buf, used.items[pj].buf_row),
                        (size_t)l.I_top * rb, cudaMemcpyDeviceToDevice, s));
   }
+  if (ctx->poison) {   // this step's half and partials are dead once its kernels are done
+    CK(cudaMemsetAsync(ctx->arena + ctx->lay.buf[buf], 0xFF, (ctx->lay.plan_rows + ctx->lay.od_rows) * rb, s));
+    CK(cudaMemsetAsync(ctx->arena + ctx->lay.ws, 0xFF, ctx->lay.ws_floats * 4, s));
+  }
   CK(cudaEventRecord(ctx->ev_step[buf], s));
   ctx->ev_step_rec[buf] = true;
   ctx->last_buf = buf;
@@ -1469,6 +1498,24 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
   ctx->ctr.pred_hits += res.pred_hits;
   ctx->ctr.pred_total += res.A.size();
   return MOEPIC_OK;
+}
+
+// The step's admissions, counters and statistics are committed (and copies into admitted slots
+// may be queued) before the kernels are launched: a failure after that point cannot be undone,
+// so it poisons the context (moepic.h: ERUNTIME -> every later call returns ESTATE).
+moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B, float* y_dev,
+                                   void* stream, uint32_t flags, moepic_trace* tr) {
+  CTX_GUARD();
+  ctx->committed = false;
+  moepic_status st = ctx->fault_at_step > 0 && ++ctx->fault_steps == ctx->fault_at_step
+                         ? inject_fault(ctx, static_cast<cudaStream_t>(stream))
+                         : layer_forward_impl(ctx, layer, h_dev, B, y_dev, stream, flags, tr);
+  if (st != MOEPIC_OK && (ctx->committed || st == MOEPIC_ERUNTIME)) {
+    ctx->poisoned = true;
+    if (st != MOEPIC_ERUNTIME) st = MOEPIC_ERUNTIME;
+  }
+  ctx->committed = false;
+  return st;
 }
 
 // host memcpy of prefill-sized buffers (tens of MB) split over the OpenMP threads
@@ -1564,15 +1611,15 @@ static size_t stats_bytes(const moepic_model_desc& d) {
   return 8 * (3 + (size_t)d.L * (2 + N + (N + 1) + (N + 1) + (N + 1) * (N + 1) + 3 * N + 1));
 }
 
-moepic_status moepic_get_stats(moepic_ctx* ctx, void* buf, size_t* bytes) {
-  CTX_GUARD();
-  if (!bytes) return fail(&ctx->err, MOEPIC_EINVAL, "bytes is NULL");
-  const size_t need = stats_bytes(ctx->desc);
+static moepic_status stats_save(const ControlPlane& cp, const moepic_model_desc& d, std::string* err, void* buf,
+                                size_t* bytes) {
+  if (!bytes) return fail(err, MOEPIC_EINVAL, "bytes is NULL");
+  const size_t need = stats_bytes(d);
   if (!buf) { *bytes = need; return MOEPIC_OK; }
-  if (*bytes < need) return fail(&ctx->err, MOEPIC_EINVAL, "buffer too small (%zu < %zu)", *bytes, need);
+  if (*bytes < need) return fail(err, MOEPIC_EINVAL, "buffer too small (%zu < %zu)", *bytes, need);
   int64_t* o = static_cast<int64_t*>(buf);
-  *o++ = ctx->desc.L; *o++ = ctx->desc.N; *o++ = ctx->desc.K;
-  for (const auto& l : ctx->cp->layers) {
+  *o++ = d.L; *o++ = d.N; *o++ = d.K;
+  for (const auto& l : cp.layers) {
     *o++ = l.st.q; *o++ = l.st.q_pred;
     for (auto v : l.st.freq) *o++ = v;
     for (auto v : l.st.rank_hit) *o++ = v;
@@ -1587,14 +1634,14 @@ moepic_status moepic_get_stats(moepic_ctx* ctx, void* buf, size_t* bytes) {
   return MOEPIC_OK;
 }
 
-moepic_status moepic_set_stats(moepic_ctx* ctx, const void* buf, size_t bytes) {
-  CTX_GUARD();
-  if (!buf || bytes != stats_bytes(ctx->desc)) return fail(&ctx->err, MOEPIC_EINVAL, "snapshot size mismatch");
+static moepic_status stats_load(ControlPlane& cp, const moepic_model_desc& d, std::string* err, const void* buf,
+                                size_t bytes) {
+  if (!buf || bytes != stats_bytes(d)) return fail(err, MOEPIC_EINVAL, "snapshot size mismatch");
   const int64_t* in = static_cast<const int64_t*>(buf);
-  if (in[0] != ctx->desc.L || in[1] != ctx->desc.N || in[2] != ctx->desc.K)
-    return fail(&ctx->err, MOEPIC_EINVAL, "snapshot shape (L, N, K) mismatch");
+  if (in[0] != d.L || in[1] != d.N || in[2] != d.K)
+    return fail(err, MOEPIC_EINVAL, "snapshot shape (L, N, K) mismatch");
   in += 3;
-  for (auto& l : ctx->cp->layers) {
+  for (auto& l : cp.layers) {
     l.st.q = *in++; l.st.q_pred = *in++;
     for (auto& v : l.st.freq) v = *in++;
     for (auto& v : l.st.rank_hit) v = *in++;
@@ -1607,6 +1654,16 @@ moepic_status moepic_set_stats(moepic_ctx* ctx, const void* buf, size_t bytes) {
     l.st.dirty = true;
   }
   return MOEPIC_OK;
+}
+
+moepic_status moepic_get_stats(moepic_ctx* ctx, void* buf, size_t* bytes) {
+  CTX_GUARD();
+  return stats_save(*ctx->cp, ctx->desc, &ctx->err, buf, bytes);
+}
+
+moepic_status moepic_set_stats(moepic_ctx* ctx, const void* buf, size_t bytes) {
+  CTX_GUARD();
+  return stats_load(*ctx->cp, ctx->desc, &ctx->err, buf, bytes);
 }
 
 moepic_status moepic_get_counters(moepic_ctx* ctx, moepic_counters* out) {
@@ -1818,6 +1875,16 @@ moepic_status moepic_hostsim_cached(moepic_hostsim* hs, int32_t layer, int32_t* 
     if (l.cached(e)) out[c++] = e;
   *n = c;
   return MOEPIC_OK;
+}
+
+moepic_status moepic_hostsim_get_stats(moepic_hostsim* hs, void* buf, size_t* bytes) {
+  if (!hs) return MOEPIC_EINVAL;
+  return stats_save(*hs->cp, hs->desc, &hs->err, buf, bytes);
+}
+
+moepic_status moepic_hostsim_set_stats(moepic_hostsim* hs, const void* buf, size_t bytes) {
+  if (!hs) return MOEPIC_EINVAL;
+  return stats_load(*hs->cp, hs->desc, &hs->err, buf, bytes);
 }
 
 const char* moepic_hostsim_last_error(const moepic_hostsim* hs) { return hs ? hs->err.c_str() : "hs is NULL"; }

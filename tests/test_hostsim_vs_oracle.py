@@ -129,3 +129,45 @@ if given is not None:
         skw = dict(use_solver=True, t_att=15.0, t_moe=30.0, t_head=5.0, t_load_exp=45.0, zeta=0.05)
         _run_pair(L, N, K, 64, I, 16, K + ub_extra, B, kw, T=24, seed=seed, n_shared=n_shared,
                   solver_at=8 if solver else None, solver_kw=skw)
+
+
+def test_stats_checkpoint_round_trip():
+    """SURVEY §5 checkpoint row: get_stats -> set_stats into a fresh control plane gives a
+    bit-identical Alg. 1 configuration (run on the restored H/P/PH and counters) and
+    identical traces afterwards, and both equal the oracle that never restarted."""
+    L, N, K, I, g = 3, 16, 2, 128, 16
+    rng = np.random.default_rng(31)
+    desc = api.model_desc(L, N, K, 64, I, row_granule=g, buffer_experts=K, max_batch=2, v_e_max=L * N)
+    a = api.HostSim(desc)
+    orc = OracleEngine(L, N, K, 64, I, row_granule=g, buffer_experts=K)
+    kw = dict(v_e=9.0, t_att=20.0, t_moe=40.0, t_head=10.0, t_load_exp=35.0, zeta=0.02, seed=4)
+    a.configure(**kw)
+    orc.configure(CacheConfig(**kw))
+    tr = _trace(rng, 70, L, N, K, 2)
+    for step in tr[:50]:
+        for i, (ids, rank) in enumerate(step):
+            a.step(i, ids, (i + 1) % L, rank)
+            orc.step(i, ids, (i + 1) % L, rank)
+    blob = a.get_stats()
+    b = api.HostSim(desc)
+    b.configure(**kw)
+    b.set_stats(blob)
+    assert b.get_stats() == blob
+    skw = dict(kw, use_solver=True)
+    ra, rb = a.configure(**skw), b.configure(**skw)
+    C, It, th, V = orc.configure(CacheConfig(**skw))
+    assert ra == rb
+    assert ra["C_i"] == C and ra["I_top_i"] == It and ra["V_i"] == V
+    for i in range(L):
+        assert a.cached(i) == b.cached(i) == orc.cache[i]
+    for step in tr[50:]:
+        for i, (ids, rank) in enumerate(step):
+            x, y = a.step(i, ids, (i + 1) % L, rank), b.step(i, ids, (i + 1) % L, rank)
+            o = orc.step(i, ids, (i + 1) % L, rank)
+            assert x.act == y.act == o.act and x.adm == y.adm == o.adm and x.plan == y.plan == o.plan
+    # a snapshot of another shape is rejected without changing the target
+    other = api.HostSim(api.model_desc(L, 8, K, 64, I, row_granule=g, max_batch=2, v_e_max=L * 8))
+    with pytest.raises(api.MoEpicError):
+        other.set_stats(blob)
+    with pytest.raises(api.MoEpicError):
+        b.set_stats(blob[:-8])
