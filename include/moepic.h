@@ -57,7 +57,9 @@ enum { MOEPIC_ADM_FREE_SLOT = -1, MOEPIC_ADM_NONE = -2 };
 /* layer_forward flags */
 enum {
   MOEPIC_FUSE_PREDICT = 1, /* run R^{(i+1) mod L} on h^i and prefetch that layer (Eq. 3)    */
-  MOEPIC_RESIDUAL = 2      /* y = h + MoE(h) instead of MoE(h) (Eq. 2's inner h + sum) */
+  MOEPIC_RESIDUAL = 2,     /* y = h + MoE(h) instead of MoE(h) (Eq. 2's inner h + sum) */
+  MOEPIC_TOKENS_SHARDED = 4 /* expert parallel with tokens sharded over the group (SURVEY §8(e),
+                              prefill config 5): see moepic_group_join                          */
 };
 
 typedef struct moepic_ctx moepic_ctx;
@@ -265,6 +267,53 @@ moepic_status moepic_attention_ws_bytes(int32_t B, int32_t S, int32_t Hq, int32_
 moepic_status moepic_attention_decode(const void* q, const void* k_cache, const void* v_cache, int32_t B,
                                       int32_t S, int32_t S_max, int32_t Hq, int32_t Hkv, int32_t dh,
                                       float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU group (expert parallel; NEXT-4: tensor parallel along I).  The ranks
+ * of one EP (ep_size > 1) or TP (tp_size > 1) layer form a group of G = ep_size or tp_size
+ * <= 8 contexts, one per process and GPU.  The data plane is the library's: either
+ *   MOEPIC_TRANSPORT_PEER: every rank's exchange region is mapped into every peer with CUDA IPC
+ *     (P2P over NVLink / NVSwitch between GPUs; also works for ranks sharing one GPU), and the
+ *     library's kernels store rows straight into the consumer's region and publish per-phase
+ *     epoch flags (release / acquire at system scope);
+ *   MOEPIC_TRANSPORT_NCCL: a communicator the library creates (ncclCommInitRank) from the
+ *     unique id in rank 0's handle: ncclAllGather / grouped ncclSend-ncclRecv / ncclAllReduce
+ *     on the compute stream (libnccl.so.2 is dlopened at join; NCCL refuses two ranks on one GPU).
+ * Joining: every rank calls moepic_group_handle, the caller all-gathers the handles with its
+ * own process group (torch.distributed: plumbing only), then every rank calls moepic_group_join
+ * with the G handles in rank order (collective: all ranks must call it).  The handle is a
+ * fixed-size opaque blob (*bytes = its size; query with out == NULL).  Blocking; EINVAL on
+ * mismatched handles (world, transport, shapes), ERUNTIME on a CUDA / NCCL failure.
+ * After a join, moepic_layer_forward on the group:
+ *   - without MOEPIC_TOKENS_SHARDED (decode: every rank passes the SAME h, B <= 32): y_dev is the
+ *     full layer output on every rank -- the partial outputs are summed over the group in rank
+ *     order inside the call (identical bits on every rank);
+ *   - with MOEPIC_TOKENS_SHARDED (EP only, n_shared == 0, no FUSE_PREDICT; rank r passes its own
+ *     B tokens, the same B on every rank, G*B <= max_batch): rank r's tokens are global tokens
+ *     [r*B, (r+1)*B).  The ranks route their own tokens, all-gather the routing (every control
+ *     plane sees the whole batch: traces / stats as if one context ran G*B tokens with ep_rank),
+ *     dispatch each token row once to every rank owning one of its experts, compute the
+ *     sub-batch there (K2 or the tcgen05 prefill GEMMs), return each rank's weighted partial sum
+ *     to the token's owner, and the owner adds them in rank order (+ h if MOEPIC_RESIDUAL).
+ *     y_dev holds rank r's B output rows.  The trace's ids / w are rank r's tokens.            */
+enum { MOEPIC_TRANSPORT_PEER = 0, MOEPIC_TRANSPORT_NCCL = 1 };
+moepic_status moepic_group_handle(moepic_ctx* ctx, int32_t transport, void* out, size_t* bytes);
+moepic_status moepic_group_join(moepic_ctx* ctx, const void* handles, size_t bytes_each);
+
+/* Host-only (no context, no GPU): the exchange lists of the token-sharded EP layer for rank
+ * `me` of G (the library computes the same lists inside layer_forward).  ids_all [G*Bl][K]
+ * routed ids of the whole batch (rank-major), experts owned by rank e*G/N.  Caller-owned
+ * outputs with the capacities below (any may be NULL); counts written to n_disp / n_sub:
+ *   d_tok / d_dst / d_row [Bl*min(G,K)]: dispatch entries (my token, destination rank, row in
+ *     the destination's sub-batch), grouped by destination, tokens ascending;
+ *   sub / c_dst / c_row [G*Bl]: the sub-batch this rank computes (global tokens ascending), and
+ *     for each of its rows the owner rank and the row in the owner's combine buffer;
+ *   r_off [Bl+1], r_row [Bl*min(G,K)]: per own token, its combine-buffer rows (owner rank asc).
+ * EINVAL on an id outside [0, N) or bad sizes.                                                  */
+moepic_status moepic_ep_plan(int32_t N, int32_t K, int32_t G, int32_t me, int32_t Bl, const int32_t* ids_all,
+                             int32_t* d_tok, int32_t* d_dst, int32_t* d_row, int32_t* n_disp,
+                             int32_t* sub, int32_t* c_dst, int32_t* c_row, int32_t* n_sub,
+                             int32_t* r_off, int32_t* r_row);
 
 const char* moepic_last_error(const moepic_ctx* ctx);   /* never NULL; "" when none           */
 void moepic_destroy(moepic_ctx* ctx);                    /* NULL is a no-op; syncs the device  */

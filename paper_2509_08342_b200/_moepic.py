@@ -21,7 +21,8 @@ OK, EINVAL, ERUNTIME, ENOMEM, ESTATE = 0, 1, 2, 3, 4
 LCP, LRU, LFU, RND = 0, 1, 2, 3
 ALPHA, BETA, GAMMA = 0, 1, 2
 ADM_FREE_SLOT, ADM_NONE = -1, -2
-FUSE_PREDICT, RESIDUAL = 1, 2
+FUSE_PREDICT, RESIDUAL, TOKENS_SHARDED = 1, 2, 4
+TRANSPORT_PEER, TRANSPORT_NCCL = 0, 1
 BF16, Q4G64 = 0, 1
 
 _i32p = C.POINTER(C.c_int32)
@@ -100,6 +101,10 @@ _sig = {
     "moepic_attention_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                           C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t,
                                           C.c_void_p]),
+    "moepic_group_handle": (C.c_int, [_ctxp, C.c_int32, C.c_void_p, C.POINTER(C.c_size_t)]),
+    "moepic_group_join": (C.c_int, [_ctxp, C.c_void_p, C.c_size_t]),
+    "moepic_ep_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i32p,
+                                 _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
     "moepic_last_error": (C.c_char_p, [_ctxp]),
     "moepic_destroy": (None, [_ctxp]),
     "moepic_hostsim_create": (C.c_int, [C.POINTER(moepic_model_desc), C.POINTER(_ctxp)]),

@@ -57,6 +57,25 @@ def pack_expert(desc, gate_bits, up_bits, down_bits) -> np.ndarray:
     return out
 
 
+def ep_plan(N, K, G, me, Bl, ids_all):
+    """moepic_ep_plan: the token-sharded EP exchange lists of rank `me` (include/moepic.h)."""
+    ids = np.ascontiguousarray(ids_all, dtype=np.int32).reshape(G * Bl, K)
+    cd, cs = Bl * min(G, K), G * Bl
+    a = {k: np.zeros(n, np.int32) for k, n in (("d_tok", cd), ("d_dst", cd), ("d_row", cd), ("sub", cs),
+                                                ("c_dst", cs), ("c_row", cs), ("r_off", Bl + 1), ("r_row", cd))}
+    nd, ns = C.c_int32(), C.c_int32()
+    _check(M.moepic_ep_plan(N, K, G, me, Bl, _ptr(ids, C.c_int32), _ptr(a["d_tok"], C.c_int32),
+                            _ptr(a["d_dst"], C.c_int32), _ptr(a["d_row"], C.c_int32), C.byref(nd),
+                            _ptr(a["sub"], C.c_int32), _ptr(a["c_dst"], C.c_int32), _ptr(a["c_row"], C.c_int32),
+                            C.byref(ns), _ptr(a["r_off"], C.c_int32), _ptr(a["r_row"], C.c_int32)), "moepic_ep_plan")
+    for k in ("d_tok", "d_dst", "d_row"):
+        a[k] = a[k][:nd.value]
+    for k in ("sub", "c_dst", "c_row"):
+        a[k] = a[k][:ns.value]
+    a["r_row"] = a["r_row"][:a["r_off"][-1]]
+    return a
+
+
 class _Cfg:
     """Keeps the numpy arrays behind a moepic_cache_config alive."""
 
@@ -215,6 +234,30 @@ class MoEpic:
         self._err(M.moepic_profile_read(self.h, kernel_class, C.byref(k)), "moepic_profile_read")
         return dict(launches=int(k.launches), total_ms=float(k.total_ms), bytes=int(k.bytes),
                     kernel_ms=float(k.kernel_ms))
+
+    def group_handle(self, transport=M.TRANSPORT_PEER) -> bytes:
+        """moepic_group_handle: this rank's opaque handle (exchange region IPC handle, NCCL id)."""
+        n = C.c_size_t()
+        self._err(M.moepic_group_handle(self.h, transport, None, C.byref(n)), "moepic_group_handle")
+        buf = C.create_string_buffer(n.value)
+        self._err(M.moepic_group_handle(self.h, transport, buf, C.byref(n)), "moepic_group_handle")
+        return buf.raw
+
+    def group_join(self, handles):
+        """moepic_group_join with the G handles in rank order (collective)."""
+        blob = b"".join(handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        self._err(M.moepic_group_join(self.h, buf, len(handles[0])), "moepic_group_join")
+
+    def join_process_group(self, transport=M.TRANSPORT_PEER, group=None):
+        """Exchange handles over an initialised torch.distributed process group (plumbing), then
+        join.  The group's rank order must match ep_rank / tp_rank."""
+        import torch
+        import torch.distributed as dist
+        mine = self.group_handle(transport)
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, mine, group=group)
+        self.group_join(out)
 
     def get_stats(self) -> bytes:
         n = C.c_size_t()

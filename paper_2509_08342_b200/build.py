@@ -23,8 +23,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu", "kernels/prefill.cu",
-              "kernels/attention.cu"]
-CXX_SOURCES = ["host/control.cpp", "moepic_api.cpp"]
+              "kernels/attention.cu", "kernels/ep.cu"]
+CXX_SOURCES = ["host/control.cpp", "host/ep_plan.cpp", "moepic_api.cpp"]
 
 
 def _depfile_deps(dep):
@@ -91,7 +91,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(o)
     if force or _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs,
-              "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
+              "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"], verbose)
     return LIB
 
 

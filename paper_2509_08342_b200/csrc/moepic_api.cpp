@@ -21,10 +21,14 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: the library dlopens libnccl.so.2 (the process's own copy) at join
 
 #include "../../include/moepic.h"
 #include "../../include/moepic_hostsim.h"
 #include "host/control.hpp"
+#include "host/ep_plan.hpp"
+#include "kernels/ep.hpp"
 #include "kernels/kernels.hpp"
 #include "kernels/prefill.hpp"
 
@@ -220,6 +224,90 @@ uint64_t plan_bytes(const Plan& p, int64_t rb) {
   return s;
 }
 
+// NCCL entry points, resolved with dlsym from the libnccl.so.2 the process already has (torch's)
+// or the system one: the library itself has no link-time NCCL dependency.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi a = [] {
+    NcclApi x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return x;
+#define NCCL_SYM(f) x.f = reinterpret_cast<decltype(x.f)>(dlsym(h, "nccl" #f))
+    NCCL_SYM(GetUniqueId); NCCL_SYM(CommInitRank); NCCL_SYM(CommDestroy); NCCL_SYM(AllGather);
+    NCCL_SYM(AllReduce); NCCL_SYM(Send); NCCL_SYM(Recv); NCCL_SYM(GroupStart); NCCL_SYM(GroupEnd);
+    NCCL_SYM(GetErrorString);
+#undef NCCL_SYM
+    x.ok = x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.AllGather && x.AllReduce && x.Send && x.Recv &&
+           x.GroupStart && x.GroupEnd && x.GetErrorString;
+    return x;
+  }();
+  return a;
+}
+
+// handle blob one rank publishes (moepic_group_handle) and every rank joins with
+struct GroupBlob {
+  uint64_t magic;
+  int32_t rank, world, transport, kind;
+  uint64_t region_bytes;
+  cudaIpcMemHandle_t ipc;
+  ncclUniqueId nccl_id;
+};
+constexpr uint64_t kGroupMagic = 0x4d6f45706963477bull;   // "MoEpicG{"
+
+// the group of ranks one context exchanges data with (EP or TP), SURVEY §8(e)
+struct Group {
+  int transport = MOEPIC_TRANSPORT_PEER;
+  int G = 1, me = 0;
+  int T_max = 0, Bl_max = 0, B_dec = 0;
+  bool joined = false;
+  uint8_t* region = nullptr;          // own exchange region (cudaMalloc: IPC-exportable)
+  EpOffsets of{};
+  EpPeers pr{};
+  bool opened[kEpMaxRanks] = {};
+  unsigned long long epoch[kEpPhases] = {};
+  int32_t* idx_h = nullptr;           // mapped pinned index lists (host writes, kernels read)
+  int32_t* idx_d = nullptr;
+  size_t idx_ints = 0;
+  ncclComm_t comm = nullptr;
+  ncclUniqueId nccl_id{};
+  std::vector<int32_t> ids_all;
+  std::vector<float> w_all;
+  EpLists lists;
+};
+
+EpOffsets ep_offsets(int G, int T_max, int Bl_max, int B_dec, int K, int d) {
+  EpOffsets o{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t r = off; off = align_up(off + bytes); return r; };
+  o.sig = take(sizeof(unsigned long long) * kEpPhases * kEpMaxRanks);
+  o.ctr = take(sizeof(unsigned int) * kEpPhases);
+  const size_t comb_rows = (size_t)Bl_max * std::min(G, K);
+  for (int h = 0; h < 2; ++h) {
+    o.ids_all[h] = take((size_t)T_max * K * 4);
+    o.w_all[h] = take((size_t)T_max * K * 4);
+    o.recv[h] = take((size_t)T_max * d * 2);
+    o.comb[h] = take(comb_rows * d * 4);
+    o.red[h] = take((size_t)G * B_dec * d * 4);
+  }
+  o.ysub = take((size_t)T_max * d * 4);
+  o.sendbuf = take(comb_rows * d * 2);
+  o.total = off;
+  return o;
+}
+
 }  // namespace
 
 // ====================================================================== context
@@ -229,6 +317,7 @@ struct moepic_ctx {
   std::unique_ptr<PfPermuteParams> pf_pp = std::make_unique<PfPermuteParams>();
   std::unique_ptr<PfGemmParams> pf_gp = std::make_unique<PfGemmParams>();
   std::unique_ptr<CombineParams> cpar = std::make_unique<CombineParams>();
+  std::unique_ptr<Group> grp;        // set by moepic_group_handle / moepic_group_join
   moepic_model_desc desc{};         // local shape: desc.I = I_full / tp_size rows per expert
   int32_t I_full = 0;               // rows per expert in the caller's (HF) tensors
   ArenaLayout lay{};
@@ -1188,8 +1277,11 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   return MOEPIC_OK;
 }
 
+// cp_ids != nullptr (token-sharded EP): the routing is already known -- ctx->ids_h holds the
+// computed sub-batch's ids (B tokens) and cp_ids / cp_B the whole batch the control plane sees.
 static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B, float* y_dev,
-                                        void* stream, uint32_t flags, moepic_trace* tr) {
+                                        void* stream, uint32_t flags, moepic_trace* tr,
+                                        const int32_t* cp_ids = nullptr, int cp_B = 0) {
   const auto& d = ctx->desc;
   if (!ctx->configured) return fail(&ctx->err, MOEPIC_EINVAL, "moepic_configure has not been called");
   if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
@@ -1215,11 +1307,17 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
 
   // ---- K1 (router + fused next-layer predictor) and the mailbox handoff
   const auto t_call = std::chrono::steady_clock::now();
-  moepic_status st = run_router(ctx, h, B, layer, predict ? j : -1, s, true, false);
+  moepic_status st = MOEPIC_OK;
+  const bool route_here = cp_ids == nullptr;
+  if (route_here) {
+    st = run_router(ctx, h, B, layer, predict ? j : -1, s, true, false);
+    ++launches;
+    cp_ids = ctx->ids_h.data();
+    cp_B = B;
+  }
   const auto t_routed = std::chrono::steady_clock::now();
   auto t_first_copy = t_routed;   // MOEPIC_HOST_TIMING
   if (st != MOEPIC_OK) return st;
-  ++launches;
 
   // ---- control plane (classification, counters, admission)
   // ---- control plane: classification first; the beta bottoms it decides are issued on
@@ -1227,7 +1325,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   // so the link starts streaming this layer's missing rows as early as possible
   StepResult res;
   const Plan* up = have_plan ? &used : nullptr;
-  cp.classify(layer, ctx->ids_h.data(), B, up, res);
+  cp.classify(layer, cp_ids, cp_B, up, res);
   const auto t_cls = std::chrono::steady_clock::now();
   if (have_plan) {
     st = finish_plan(ctx, used, res);
@@ -1251,14 +1349,20 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   int64_t od_row = 0;
   int n_od = 0;
   bool waited = false;
-  // The step's last on-demand copy is split (decode): every copy of more than
-  // tail_rows + 1 rows is issued at once except its final tail_rows rows, which are held; a later
-  // copy releases the held tail first.  At the end the held tail (if any) is the step's last
-  // copy: ev_od_head marks "everything but that tail landed" and the K2 launch over the rest
-  // runs while the tail is in flight.
-  struct HeldTail { uint8_t* dst; const uint8_t* src; size_t bytes; int32_t rows; } held{nullptr, nullptr, 0, 0};
+  // The step's last on-demand copy is split into head + tail (decode): which copy is last is
+  // known from the classification alone (pass 1: beta / gamma bottoms, pass 2: gamma tops), so
+  // that copy is issued as head, ev_od_head, tail right away -- nothing is held back, and the
+  // K2 launch over everything but the tail runs while the tail is in flight.
+  int n_copies = 0;
+  for (size_t a = 0; a < res.A.size(); ++a) {
+    if (res.plan_idx[a] >= 0) continue;
+    const int c = res.cls[a];
+    if (c == kBeta || (c == kGamma && l.I_top < d.I)) ++n_copies;
+    if (c == kGamma && l.I_top > 0) ++n_copies;
+  }
   const bool split_ok = B <= kDecodeMaxB && ctx->od_tail_bytes > 0;
   const int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
+  const uint8_t* split_dst = nullptr;   // segment whose tail was split off
   auto copy = [&](uint8_t* dst, const uint8_t* src, int32_t rows, bool evicted = false) -> moepic_status {
     const size_t bytes = (size_t)rows * rb;
     const auto tw0 = std::chrono::steady_clock::now();
@@ -1269,16 +1373,13 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     }
     const auto tw1 = std::chrono::steady_clock::now();
     if (evicted && ctx->poison) CK(cudaMemsetAsync(dst, 0xFF, bytes, ctx->copy));   // the victim's old top
-    if (held.bytes) {   // a later copy exists: the held tail is not the step's last
-      CK(cudaMemcpyAsync(held.dst, held.src, held.bytes, cudaMemcpyHostToDevice, ctx->copy));
-      ctx->ctr.h2d_copies++;
-      held = HeldTail{nullptr, nullptr, 0, 0};
-    }
-    if (split_ok && (int64_t)rows > 2 * tail_rows_split) {
+    if (split_ok && n_od == n_copies - 1 && (int64_t)rows > 2 * tail_rows_split) {
       const size_t head = bytes - (size_t)tail_rows_split * rb;
       CK(cudaMemcpyAsync(dst, src, head, cudaMemcpyHostToDevice, ctx->copy));
-      ctx->ctr.h2d_copies++;
-      held = HeldTail{dst + head, src + head, bytes - head, (int32_t)tail_rows_split};
+      CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
+      CK(cudaMemcpyAsync(dst + head, src + head, bytes - head, cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies += 2;
+      split_dst = dst;
     } else {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies++;
@@ -1320,7 +1421,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     }
   }
   const auto t_p1 = std::chrono::steady_clock::now();
-  cp.commit(layer, ctx->ids_h.data(), B, up, res);
+  cp.commit(layer, cp_ids, cp_B, up, res);
   ctx->committed = true;   // from here on, any failure leaves slots admitted with no landed rows
   const auto t_com = std::chrono::steady_clock::now();
   if (ctx->host_timing) {
@@ -1347,22 +1448,19 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     if ((st = copy(top, ctx->host_expert(layer, e), l.I_top, slot >= 0)) != MOEPIC_OK) return st;
     gC.push_back(StepSeg{top, e, l.I_top, masks[a], 0});
   }
-  // the step's last on-demand copy, if its tail is held: an event, then the tail (gC's last entry
-  // is the segment the held tail belongs to: copy() runs right before each gC push)
+  // the split copy's segment is the last one pushed to gC: cut its tail into its own segment
   const uint8_t* tail_base = nullptr;
-  if (held.bytes) {
+  if (split_dst) {
     StepSeg& last = gC.back();
-    CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
-    CK(cudaMemcpyAsync(held.dst, held.src, held.bytes, cudaMemcpyHostToDevice, ctx->copy));
-    ctx->ctr.h2d_copies++;
+    if (last.base != split_dst || n_od != n_copies)
+      return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: split copy is not the step's last on-demand segment");
     StepSeg tail = last;
-    last.nrows -= held.rows;
-    tail.base = held.dst;
-    tail.nrows = held.rows;
+    last.nrows -= (int32_t)tail_rows_split;
+    tail.base = split_dst + (size_t)last.nrows * rb;
+    tail.nrows = (int32_t)tail_rows_split;
     tail.row0 = last.row0 + last.nrows;
     gC.push_back(tail);
     tail_base = tail.base;
-    held = HeldTail{nullptr, nullptr, 0, 0};
   }
   if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
   {   // an expert's on-demand segments consecutive, tops first (the prefill down GEMM groups by expert)
@@ -1489,7 +1587,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     tr->kernel_launches = launches;
   }
   ctx->ctr.layer_steps++;
-  ctx->ctr.kernel_launches += launches - 1;   // router already counted
+  ctx->ctr.kernel_launches += launches - (route_here ? 1 : 0);   // run_router counts its own
   ctx->ctr.pcie_ondemand_bytes += res.pcie_ondemand;
   ctx->ctr.hbm_bytes += hbm;
   ctx->ctr.act_alpha += res.alpha;
@@ -1500,6 +1598,303 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   return MOEPIC_OK;
 }
 
+// ====================================================================== multi-GPU group
+#define NCK(call)                                                                          \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess) {                                                               \
+      ctx->poisoned = true;                                                                \
+      return fail(&ctx->err, MOEPIC_ERUNTIME, "%s: %s", #call, nccl_api().GetErrorString(r_)); \
+    }                                                                                      \
+  } while (0)
+
+static int group_size(const moepic_model_desc& d) { return d.ep_size > 1 ? d.ep_size : d.tp_size; }
+static int group_rank(const moepic_model_desc& d) { return d.ep_size > 1 ? d.ep_rank : d.tp_rank; }
+
+static inline int ep_grid(int64_t warps_of_work) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((warps_of_work + 7) / 8, 2 * kSMs));
+}
+
+// replicated-token group (decode EP / TP): y <- sum over ranks of the partial outputs
+static moepic_status group_allreduce(moepic_ctx* ctx, float* y, int B, cudaStream_t s) {
+  Group& g = *ctx->grp;
+  const int n = B * ctx->desc.d;
+  if (g.transport == MOEPIC_TRANSPORT_NCCL) {
+    NCK(nccl_api().AllReduce(y, y, (size_t)n, ncclFloat32, ncclSum, g.comm, s));
+    return MOEPIC_OK;
+  }
+  EpAllreduceParams p{};
+  p.pr = g.pr; p.of = g.of; p.y = y; p.n = n; p.slot_floats = g.B_dec * ctx->desc.d;
+  p.epoch = ++g.epoch[kEpPhReduce];
+  launch_ep_allreduce(p, (int)std::min<int64_t>(32, std::max<int64_t>(1, (n / 4 + 255) / 256)), s);
+  CK(cudaGetLastError());
+  ctx->ctr.kernel_launches++;
+  return MOEPIC_OK;
+}
+
+// token-sharded EP layer: route own tokens -> all-gather routing ->
+// dispatch rows to the experts' ranks -> compute the sub-batch -> combine back -> reduce
+static moepic_status sharded_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t Bl, float* y_dev,
+                                     void* stream, uint32_t flags, moepic_trace* tr) {
+  const auto& d = ctx->desc;
+  Group& g = *ctx->grp;
+  const int G = g.G, K = d.K, T = G * Bl;
+  if (!ctx->configured) return fail(&ctx->err, MOEPIC_EINVAL, "moepic_configure has not been called");
+  if (layer < 0 || layer >= d.L) return fail(&ctx->err, MOEPIC_EINVAL, "layer out of range");
+  if (d.ep_size < 2) return fail(&ctx->err, MOEPIC_EINVAL, "MOEPIC_TOKENS_SHARDED needs an expert-parallel group");
+  if (d.n_shared) return fail(&ctx->err, MOEPIC_EINVAL, "MOEPIC_TOKENS_SHARDED needs n_shared == 0");
+  if (flags & MOEPIC_FUSE_PREDICT) return fail(&ctx->err, MOEPIC_EINVAL, "MOEPIC_TOKENS_SHARDED excludes FUSE_PREDICT");
+  if (Bl < 1 || T > d.max_batch || Bl > g.Bl_max) return fail(&ctx->err, MOEPIC_EINVAL, "B must be in [1, max_batch / G]");
+  if (!h_dev || !y_dev || (reinterpret_cast<uintptr_t>(h_dev) & 15) || (reinterpret_cast<uintptr_t>(y_dev) & 15))
+    return fail(&ctx->err, MOEPIC_EINVAL, "h_dev / y_dev must be 16-byte aligned device pointers");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint16_t* h = static_cast<const uint16_t*>(h_dev);
+  const bool nccl = g.transport == MOEPIC_TRANSPORT_NCCL;
+  const NcclApi& nc = nccl_api();
+  int32_t* ids_loc = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.ids);
+  float* w_loc = reinterpret_cast<float*>(ctx->arena + ctx->lay.w);
+
+  // ---- route my tokens, gather the batch's routing on every rank, publish it to the host
+  moepic_status st = run_router(ctx, h, Bl, layer, -1, s, false, false);
+  if (st != MOEPIC_OK) return st;
+  const unsigned long long e_ids = ++g.epoch[kEpPhIds];
+  const int half = (int)(e_ids & 1);
+  if (nccl) {
+    NCK(nc.GroupStart());
+    NCK(nc.AllGather(ids_loc, g.region + g.of.ids_all[half], (size_t)Bl * K, ncclInt32, g.comm, s));
+    NCK(nc.AllGather(w_loc, g.region + g.of.w_all[half], (size_t)Bl * K, ncclFloat32, g.comm, s));
+    NCK(nc.GroupEnd());
+  }
+  EpIdsParams ip{};
+  ip.pr = g.pr; ip.of = g.of; ip.ids = ids_loc; ip.w = w_loc; ip.BlK = Bl * K; ip.TK = T * K;
+  ip.push = nccl ? 0 : 1; ip.epoch = e_ids;
+  const size_t BK = (size_t)d.max_batch * K;
+  ip.mb_ids = reinterpret_cast<unsigned long long*>(ctx->mailbox_dev + 64);
+  ip.mb_w = ip.mb_ids + BK;
+  ip.seq = ++ctx->seq;
+  launch_ep_ids(ip, s);
+  CK(cudaGetLastError());
+  ctx->ctr.kernel_launches++;
+  if ((st = wait_mailbox(ctx, s, 0, (size_t)T * K)) != MOEPIC_OK) return st;
+  if ((st = wait_mailbox(ctx, s, BK, (size_t)T * K)) != MOEPIC_OK) return st;
+  {
+    const uint64_t* words = reinterpret_cast<const uint64_t*>(ctx->mailbox + 64);
+    for (int i = 0; i < T * K; ++i) {
+      g.ids_all[i] = (int32_t)(uint32_t)words[i];
+      const uint32_t wb = (uint32_t)words[BK + i];
+      memcpy(&g.w_all[i], &wb, 4);
+    }
+  }
+  // ---- exchange lists (host, mapped memory; the previous layer's readers are done: this
+  // layer's routing kernel ran after them on the same stream)
+  EpLists& L = g.lists;
+  if (!ep_plan(g.ids_all.data(), d.N, K, G, g.me, Bl, L))
+    return fail(&ctx->err, MOEPIC_ERUNTIME, "routing produced an expert id out of range");
+  const int n_disp = (int)L.d_tok.size(), n_sub = (int)L.sub.size();
+  const size_t cap_d = (size_t)g.Bl_max * std::min(G, K), cap_s = (size_t)g.T_max;
+  int32_t* I = g.idx_h;
+  int32_t *dt = I, *dd = dt + cap_d, *dr = dd + cap_d, *sb = dr + cap_d, *cd = sb + cap_s, *cr = cd + cap_s,
+          *ro = cr + cap_s, *rr = ro + g.Bl_max + 1;
+  std::copy(L.d_tok.begin(), L.d_tok.end(), dt);
+  std::copy(L.d_dst.begin(), L.d_dst.end(), dd);
+  std::copy(L.d_row.begin(), L.d_row.end(), dr);
+  std::copy(L.sub.begin(), L.sub.end(), sb);
+  std::copy(L.c_dst.begin(), L.c_dst.end(), cd);
+  std::copy(L.c_row.begin(), L.c_row.end(), cr);
+  std::copy(L.r_off.begin(), L.r_off.end(), ro);
+  std::copy(L.r_row.begin(), L.r_row.end(), rr);
+  std::atomic_thread_fence(std::memory_order_release);
+  auto dev = [&](int32_t* hp) { return g.idx_d + (hp - g.idx_h); };
+
+  // ---- dispatch: my rows to the ranks owning their experts; the sub-batch routing to the arena
+  const unsigned long long e_disp = ++g.epoch[kEpPhDispatch];
+  const int hd = (int)(e_disp & 1);
+  EpDispatchParams dp{};
+  dp.pr = g.pr; dp.of = g.of; dp.h = h; dp.d = d.d; dp.K = K; dp.push = nccl ? 0 : 1;
+  dp.n_disp = n_disp; dp.d_tok = dev(dt); dp.d_dst = dev(dd); dp.d_row = dev(dr);
+  dp.sendbuf = reinterpret_cast<uint16_t*>(g.region + g.of.sendbuf);
+  dp.n_sub = n_sub; dp.sub = dev(sb); dp.ids_out = ids_loc; dp.w_out = w_loc; dp.epoch = e_disp;
+  launch_ep_dispatch(dp, ep_grid(std::max(n_disp, (n_sub * K + 31) / 32)), s);
+  CK(cudaGetLastError());
+  ctx->ctr.kernel_launches++;
+  const uint16_t* hsub = reinterpret_cast<const uint16_t*>(g.region + g.of.recv[hd]);
+  if (nccl) {
+    NCK(nc.GroupStart());
+    size_t soff = 0, roff = 0;
+    for (int q = 0; q < G; ++q) {
+      if (L.n_send[q]) NCK(nc.Send(dp.sendbuf + soff * d.d, (size_t)L.n_send[q] * d.d, ncclBfloat16, q, g.comm, s));
+      if (L.n_recv[q])
+        NCK(nc.Recv(g.region + g.of.recv[hd] + roff * d.d * 2, (size_t)L.n_recv[q] * d.d, ncclBfloat16, q, g.comm, s));
+      soff += L.n_send[q];
+      roff += L.n_recv[q];
+    }
+    NCK(nc.GroupEnd());
+  } else {
+    launch_ep_wait(g.pr, g.of, kEpPhDispatch, e_disp, s);
+    CK(cudaGetLastError());
+    ctx->ctr.kernel_launches++;
+  }
+
+  // ---- the sub-batch through the split-expert path (control plane sees all T tokens)
+  float* ysub = reinterpret_cast<float*>(g.region + g.of.ysub);
+  for (int i = 0; i < n_sub * K; ++i) ctx->ids_h[i] = g.ids_all[(size_t)L.sub[i / K] * K + i % K];
+  if (n_sub > 0) {
+    st = layer_forward_impl(ctx, layer, hsub, n_sub, ysub, stream, 0, tr, g.ids_all.data(), T);
+    if (st != MOEPIC_OK) return st;
+  } else {   // no token routes here: the control plane still sees the step (counters, stats)
+    StepResult res;
+    Plan used;
+    const bool have_plan = ctx->pending.valid && ctx->pending.target == layer;
+    if (have_plan) used = std::move(ctx->pending);
+    ctx->pending = Plan();
+    ctx->cp->step(layer, g.ids_all.data(), T, have_plan ? &used : nullptr, res);
+    ctx->committed = true;
+    fill_step_trace(tr, res, nullptr);
+    ctx->ctr.layer_steps++;
+  }
+
+  // ---- combine: partial rows back to the token owners, owners reduce in rank order
+  const unsigned long long e_comb = ++g.epoch[kEpPhCombine];
+  const int hc = (int)(e_comb & 1);
+  if (nccl) {
+    NCK(nc.GroupStart());
+    size_t soff = 0, roff = 0;
+    for (int q = 0; q < G; ++q) {
+      if (L.n_recv[q]) NCK(nc.Send(ysub + soff * d.d, (size_t)L.n_recv[q] * d.d, ncclFloat32, q, g.comm, s));
+      if (L.n_send[q])
+        NCK(nc.Recv(g.region + g.of.comb[hc] + roff * d.d * 4, (size_t)L.n_send[q] * d.d, ncclFloat32, q, g.comm, s));
+      soff += L.n_recv[q];
+      roff += L.n_send[q];
+    }
+    NCK(nc.GroupEnd());
+  } else {
+    EpCombineParams cpp{};
+    cpp.pr = g.pr; cpp.of = g.of; cpp.ysub = ysub; cpp.d = d.d; cpp.n_sub = n_sub;
+    cpp.c_dst = dev(cd); cpp.c_row = dev(cr); cpp.epoch = e_comb;
+    launch_ep_combine(cpp, ep_grid(n_sub), s);
+    CK(cudaGetLastError());
+    ctx->ctr.kernel_launches++;
+  }
+  EpReduceParams rp{};
+  rp.pr = g.pr; rp.of = g.of; rp.h = h; rp.y = y_dev; rp.d = d.d; rp.Bl = Bl;
+  rp.residual = (flags & MOEPIC_RESIDUAL) ? 1 : 0; rp.wait = nccl ? 0 : 1;
+  rp.r_off = dev(ro); rp.r_row = dev(rr); rp.epoch = e_comb;
+  launch_ep_reduce(rp, (int)std::min<int64_t>(2 * kSMs, std::max<int64_t>(1, ((int64_t)Bl * d.d / 4 + 255) / 256)), s);
+  CK(cudaGetLastError());
+  ctx->ctr.kernel_launches++;
+  if (tr) {   // the caller's own tokens
+    for (int i = 0; i < Bl * K; ++i) {
+      if (tr->ids) tr->ids[i] = g.ids_all[(size_t)g.me * Bl * K + i];
+      if (tr->w) tr->w[i] = g.w_all[(size_t)g.me * Bl * K + i];
+    }
+  }
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_group_handle(moepic_ctx* ctx, int32_t transport, void* out, size_t* bytes) {
+  CTX_GUARD();
+  const auto& d = ctx->desc;
+  if (!bytes) return fail(&ctx->err, MOEPIC_EINVAL, "bytes is NULL");
+  if (!out) { *bytes = sizeof(GroupBlob); return MOEPIC_OK; }
+  if (*bytes < sizeof(GroupBlob)) return fail(&ctx->err, MOEPIC_EINVAL, "handle buffer too small");
+  const int G = group_size(d);
+  if (G < 2 || G > kEpMaxRanks) return fail(&ctx->err, MOEPIC_EINVAL, "a group needs ep_size or tp_size in [2, 8]");
+  if (transport != MOEPIC_TRANSPORT_PEER && transport != MOEPIC_TRANSPORT_NCCL)
+    return fail(&ctx->err, MOEPIC_EINVAL, "unknown transport");
+  if (transport == MOEPIC_TRANSPORT_NCCL && !nccl_api().ok)
+    return fail(&ctx->err, MOEPIC_EINVAL, "libnccl.so.2 could not be loaded");
+  if (ctx->grp && ctx->grp->joined) return fail(&ctx->err, MOEPIC_EINVAL, "already joined");
+  if (!ctx->grp) {
+    auto g = std::make_unique<Group>();
+    g->G = G;
+    g->me = group_rank(d);
+    g->T_max = d.max_batch;
+    g->Bl_max = (d.max_batch + G - 1) / G;
+    g->B_dec = std::min(d.max_batch, kDecodeMaxB);
+    g->of = ep_offsets(G, g->T_max, g->Bl_max, g->B_dec, d.K, d.d);
+    if (cudaMalloc(&g->region, g->of.total) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(&ctx->err, MOEPIC_ENOMEM, "exchange region (%zu bytes)", g->of.total);
+    }
+    CK(cudaMemset(g->region, 0, g->of.sig + 0 + (g->of.ctr - g->of.sig) + sizeof(unsigned int) * kEpPhases));
+    g->idx_ints = 3 * (size_t)g->Bl_max * std::min(G, d.K) + 3 * (size_t)g->T_max + g->Bl_max + 1 +
+                  (size_t)g->Bl_max * std::min(G, d.K) + 64;
+    if (cudaHostAlloc(&g->idx_h, g->idx_ints * 4, cudaHostAllocMapped) != cudaSuccess) {
+      cudaFree(g->region);
+      return fail(&ctx->err, MOEPIC_ENOMEM, "index lists (mapped pinned)");
+    }
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->idx_d), g->idx_h, 0));
+    g->ids_all.assign((size_t)g->T_max * d.K, 0);
+    g->w_all.assign((size_t)g->T_max * d.K, 0.f);
+    g->pr.G = G;
+    g->pr.me = g->me;
+    g->pr.base[g->me] = g->region;
+    if (transport == MOEPIC_TRANSPORT_NCCL && g->me == 0) NCK(nccl_api().GetUniqueId(&g->nccl_id));
+    ctx->grp = std::move(g);
+  }
+  ctx->grp->transport = transport;
+  GroupBlob b{};
+  b.magic = kGroupMagic;
+  b.rank = ctx->grp->me;
+  b.world = G;
+  b.transport = transport;
+  b.kind = d.ep_size > 1 ? 0 : 1;
+  b.region_bytes = ctx->grp->of.total;
+  CK(cudaIpcGetMemHandle(&b.ipc, ctx->grp->region));
+  b.nccl_id = ctx->grp->nccl_id;
+  memcpy(out, &b, sizeof b);
+  *bytes = sizeof b;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_group_join(moepic_ctx* ctx, const void* handles, size_t bytes_each) {
+  CTX_GUARD();
+  if (!ctx->grp) return fail(&ctx->err, MOEPIC_EINVAL, "moepic_group_handle has not been called");
+  Group& g = *ctx->grp;
+  if (g.joined) return fail(&ctx->err, MOEPIC_EINVAL, "already joined");
+  if (!handles || bytes_each != sizeof(GroupBlob)) return fail(&ctx->err, MOEPIC_EINVAL, "handle size mismatch");
+  std::vector<GroupBlob> bl(g.G);
+  for (int r = 0; r < g.G; ++r) {
+    memcpy(&bl[r], static_cast<const uint8_t*>(handles) + (size_t)r * bytes_each, sizeof(GroupBlob));
+    const GroupBlob& b = bl[r];
+    if (b.magic != kGroupMagic || b.rank != r || b.world != g.G || b.transport != g.transport ||
+        b.region_bytes != g.of.total || b.kind != (ctx->desc.ep_size > 1 ? 0 : 1))
+      return fail(&ctx->err, MOEPIC_EINVAL, "handle %d does not match this group (rank, world, transport, shape)", r);
+  }
+  if (g.transport == MOEPIC_TRANSPORT_PEER) {
+    for (int r = 0; r < g.G; ++r) {
+      if (r == g.me) continue;
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, bl[r].ipc, cudaIpcMemLazyEnablePeerAccess));
+      g.pr.base[r] = static_cast<uint8_t*>(p);
+      g.opened[r] = true;
+    }
+  } else {
+    NCK(nccl_api().CommInitRank(&g.comm, g.G, bl[0].nccl_id, g.me));
+    for (int r = 0; r < g.G; ++r) g.pr.base[r] = g.region;   // kernels only touch base[me]
+  }
+  CK(cudaDeviceSynchronize());
+  g.joined = true;
+  return MOEPIC_OK;
+}
+
+moepic_status moepic_ep_plan(int32_t N, int32_t K, int32_t G, int32_t me, int32_t Bl, const int32_t* ids_all,
+                             int32_t* d_tok, int32_t* d_dst, int32_t* d_row, int32_t* n_disp,
+                             int32_t* sub, int32_t* c_dst, int32_t* c_row, int32_t* n_sub,
+                             int32_t* r_off, int32_t* r_row) {
+  if (N < 2 || K < 1 || K >= N || G < 1 || G > kEpMaxRanks || N % G || me < 0 || me >= G || Bl < 1 || !ids_all)
+    return MOEPIC_EINVAL;
+  EpLists o;
+  if (!ep_plan(ids_all, N, K, G, me, Bl, o)) return MOEPIC_EINVAL;
+  auto put = [](int32_t* dst, const std::vector<int32_t>& v) { if (dst) std::copy(v.begin(), v.end(), dst); };
+  put(d_tok, o.d_tok); put(d_dst, o.d_dst); put(d_row, o.d_row);
+  put(sub, o.sub); put(c_dst, o.c_dst); put(c_row, o.c_row);
+  put(r_off, o.r_off); put(r_row, o.r_row);
+  if (n_disp) *n_disp = (int32_t)o.d_tok.size();
+  if (n_sub) *n_sub = (int32_t)o.sub.size();
+  return MOEPIC_OK;
+}
+
 // The step's admissions, counters and statistics are committed (and copies into admitted slots
 // may be queued) before the kernels are launched: a failure after that point cannot be undone,
 // so it poisons the context (moepic.h: ERUNTIME -> every later call returns ESTATE).
@@ -1507,9 +1902,20 @@ moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h
                                    void* stream, uint32_t flags, moepic_trace* tr) {
   CTX_GUARD();
   ctx->committed = false;
-  moepic_status st = ctx->fault_at_step > 0 && ++ctx->fault_steps == ctx->fault_at_step
-                         ? inject_fault(ctx, static_cast<cudaStream_t>(stream))
-                         : layer_forward_impl(ctx, layer, h_dev, B, y_dev, stream, flags, tr);
+  const bool grouped = ctx->grp && ctx->grp->joined;
+  if ((flags & MOEPIC_TOKENS_SHARDED) && !grouped)
+    return fail(&ctx->err, MOEPIC_EINVAL, "MOEPIC_TOKENS_SHARDED needs a joined group");
+  if (grouped && !(flags & MOEPIC_TOKENS_SHARDED) && B > kDecodeMaxB)
+    return fail(&ctx->err, MOEPIC_EINVAL, "replicated tokens over a group need B <= 32 (use MOEPIC_TOKENS_SHARDED)");
+  moepic_status st;
+  if (ctx->fault_at_step > 0 && ++ctx->fault_steps == ctx->fault_at_step) {
+    st = inject_fault(ctx, static_cast<cudaStream_t>(stream));
+  } else if (flags & MOEPIC_TOKENS_SHARDED) {
+    st = sharded_forward(ctx, layer, h_dev, B, y_dev, stream, flags, tr);
+  } else {
+    st = layer_forward_impl(ctx, layer, h_dev, B, y_dev, stream, flags, tr);
+    if (st == MOEPIC_OK && grouped) st = group_allreduce(ctx, y_dev, B, static_cast<cudaStream_t>(stream));
+  }
   if (st != MOEPIC_OK && (ctx->committed || st == MOEPIC_ERUNTIME)) {
     ctx->poisoned = true;
     if (st != MOEPIC_ERUNTIME) st = MOEPIC_ERUNTIME;
@@ -1763,6 +2169,14 @@ void moepic_destroy(moepic_ctx* ctx) {
               "pred_topk %.2f ranked %.2f end %.2f us\n", cnt, acc[1] / cnt, acc[2] / cnt, acc[5] / cnt,
               acc[3] / cnt, acc[6] / cnt, acc[7] / cnt, acc[4] / cnt);
     cudaFree(ctx->k1dbg);
+  }
+  if (ctx->grp) {
+    Group& g = *ctx->grp;
+    for (int r = 0; r < kEpMaxRanks; ++r)
+      if (g.opened[r]) cudaIpcCloseMemHandle(g.pr.base[r]);
+    if (g.comm) nccl_api().CommDestroy(g.comm);
+    if (g.region) cudaFree(g.region);
+    if (g.idx_h) cudaFreeHost(g.idx_h);
   }
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   for (auto e : ctx->feed_ev)

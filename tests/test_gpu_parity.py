@@ -200,7 +200,7 @@ def test_od_tail_split(B, tail_kb, monkeypatch):
         ctx = _ctx(m, max_batch=B, v_e_max=128.0)
         orc = OracleEngine(2, S.N, S.K, S.d, S.I)
         cfg = dict(v_e=128.0, seed=5)
-        ctx.configure(**cfg)
+        ctx.configure(**cfg, cancel_prefetch=False)   # every planned chunk issued: a timing-free count
         orc.configure(CacheConfig(**cfg))
         c0 = ctx.counters()
         _replay(m, ctx, orc, toks, api.M.FUSE_PREDICT)
