@@ -129,6 +129,13 @@ typedef struct {
                               dropped ("terminates the prefetch operation").  Plans,
                               classes and traces are unchanged; only the bytes actually moved
                               (moepic_counters) differ.  0: every planned byte is transferred.  */
+  const int64_t* prefetch_rows_i; /* [L] prefetch window W_i in expert rows, or NULL.  Reading Q30
+                              (DESIGN.md): the plan for layer i is cut at min(U_b*I, W_i) rows
+                              and the bottom at the cut keeps its first g*floor(rest/g) rows --
+                              the deterministic form of "the router terminates the prefetch"
+                              (P:291); an activated expert with such a prefix is beta and loads
+                              only the rest of its bottom.  With a window, Alg. 1's Y_i is not a
+                              planner cap (y_cap_i still is).  EINVAL if any W_i < 0.          */
 } moepic_cache_config;
 
 /* configure output: caller-owned arrays of length L (any may be NULL) */

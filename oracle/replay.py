@@ -21,6 +21,12 @@ Per step, in order:
   7. plan for the next layer (Q7/Q8): walk R'; rows = I - I_top if the top is
      cached there (skip if 0) else I (full); stop at the first item that does not fit
      U_b * I rows or when the count reaches the Y cap.
+     Reading Q30 (window-capped plan): with a per-layer prefetch window W_j in rows
+     (prefetch_rows_i), the plan is cut at min(U_b * I, W_j) rows; the count cap is then
+     y_cap only (Alg. 1's Y stays inside the solver).  The item at the cut, if it is a
+     bottom, keeps its first g * floor(remaining / g) rows: "the router terminates the
+     prefetch" mid-item, deterministically at W_j.  An activated expert whose bottom
+     prefix was prefetched is beta (not fully resident) and loads only the rest.
 """
 from __future__ import annotations
 
@@ -55,6 +61,7 @@ class CacheConfig:
     y_cap_i: list | None = None
     prefetch: bool = True
     seed: int = 0
+    prefetch_rows_i: list | None = None   # reading Q30: per-layer window W_j in rows
 
 
 @dataclass
@@ -185,7 +192,10 @@ class OracleEngine:
             return Plan(j, [], ranking)
         cap_rows = self.U_b * self.I
         ycap = self.N if cfg.y_cap_i is None else cfg.y_cap_i[j]
-        if self.Y is not None:
+        window = cfg.prefetch_rows_i is not None
+        if window:
+            cap_rows = min(cap_rows, cfg.prefetch_rows_i[j])
+        elif self.Y is not None:
             ycap = min(ycap, self.Y[j])
         items, used = [], 0
         for e in ranking:
@@ -202,6 +212,9 @@ class OracleEngine:
             else:
                 rows, full = self.I, True
             if used + rows > cap_rows:
+                part = self.g * ((cap_rows - used) // self.g)
+                if window and not full and part > 0:      # Q30: the cut bottom keeps its prefix
+                    items.append((e, False, part))
                 break
             items.append((e, full, rows))
             used += rows
@@ -240,7 +253,8 @@ class OracleEngine:
         for e in A:
             cached = on and e in self.cache[i]
             p = planned.get(e)
-            if (cached and (self.I_top[i] == I or (p is not None and not p[0]))) or (p is not None and p[0]):
+            whole_bottom = p is not None and not p[0] and p[1] == I - self.I_top[i]
+            if (cached and (self.I_top[i] == I or whole_bottom)) or (p is not None and p[0]):
                 c = ALPHA
             elif cached:
                 c = BETA
@@ -287,8 +301,9 @@ class OracleEngine:
         # 6. bytes
         rb = self.row_bytes
         for e in A:
-            if cls[e] == BETA:
-                tr.pcie_ondemand += (I - self.I_top[i]) * rb
+            if cls[e] == BETA:   # minus a prefetched bottom prefix (Q30)
+                pre = planned[e][1] if e in planned and not planned[e][0] else 0
+                tr.pcie_ondemand += (I - self.I_top[i] - pre) * rb
             elif cls[e] == GAMMA:
                 tr.pcie_ondemand += I * rb
         # 7. plan next layer

@@ -45,7 +45,7 @@ class moepic_cache_config(C.Structure):
                 ("policy", C.c_int32), ("rho", C.c_double), ("omega", C.c_int32), ("zeta", C.c_double),
                 ("t_att", C.c_double), ("t_moe", C.c_double), ("t_head", C.c_double),
                 ("t_load_exp", C.c_double), ("y_cap_i", _i32p), ("prefetch", C.c_int32),
-                ("seed", C.c_uint64), ("cancel_prefetch", C.c_int32)]
+                ("seed", C.c_uint64), ("cancel_prefetch", C.c_int32), ("prefetch_rows_i", C.POINTER(C.c_int64))]
 
 
 class moepic_config_out(C.Structure):

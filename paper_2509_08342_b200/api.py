@@ -81,16 +81,17 @@ class _Cfg:
 
     def __init__(self, L, v_e, v_i=None, theta_i=None, use_solver=False, policy=M.LCP, rho=0.25,
                  omega=128, zeta=0.01, t_att=0.0, t_moe=0.0, t_head=0.0, t_load_exp=0.0, y_cap_i=None,
-                 prefetch=True, seed=0, cancel_prefetch=True):
+                 prefetch=True, seed=0, cancel_prefetch=True, prefetch_rows_i=None):
         self.v_i = None if v_i is None else np.ascontiguousarray(v_i, dtype=np.float64)
         self.th = None if theta_i is None else np.ascontiguousarray(theta_i, dtype=np.float64)
         self.yc = None if y_cap_i is None else np.ascontiguousarray(y_cap_i, dtype=np.int32)
+        self.pw = None if prefetch_rows_i is None else np.ascontiguousarray(prefetch_rows_i, dtype=np.int64)
         self.c = M.moepic_cache_config(
             v_e=float(v_e), v_i=_ptr(self.v_i, C.c_double), theta_i=_ptr(self.th, C.c_double),
             use_solver=int(use_solver), policy=int(policy), rho=float(rho), omega=int(omega),
             zeta=float(zeta), t_att=float(t_att), t_moe=float(t_moe), t_head=float(t_head),
             t_load_exp=float(t_load_exp), y_cap_i=_ptr(self.yc, C.c_int32), prefetch=int(prefetch),
-            seed=int(seed), cancel_prefetch=int(cancel_prefetch))
+            seed=int(seed), cancel_prefetch=int(cancel_prefetch), prefetch_rows_i=_ptr(self.pw, C.c_int64))
         self.C_i = np.zeros(L, np.int32)
         self.I_top = np.zeros(L, np.int32)
         self.theta_eff = np.zeros(L, np.float64)

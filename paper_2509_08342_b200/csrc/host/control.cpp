@@ -234,6 +234,9 @@ std::string ControlPlane::configure(const CacheParams& p, uint64_t slot_pool_row
   if (!p.v_i.empty() && (int)p.v_i.size() != L) return "v_i must have L entries";
   if (!p.theta_i.empty() && (int)p.theta_i.size() != L) return "theta_i must have L entries";
   if (!p.y_cap.empty() && (int)p.y_cap.size() != L) return "y_cap_i must have L entries";
+  if (!p.pf_rows.empty() && (int)p.pf_rows.size() != L) return "prefetch_rows_i must have L entries";
+  for (int64_t w : p.pf_rows)
+    if (w < 0) return "prefetch_rows_i must be >= 0";
   std::vector<double> Vnew;
   std::vector<double> thetas;
   std::vector<int> Cs(L);
@@ -349,7 +352,9 @@ void ControlPlane::classify(int layer, const int32_t* ids, int B, const Plan* pl
   for (int e : out.A) {
     bool cached = l.cached(e);
     int pj = pidx[e];
-    bool p_bottom = pj >= 0 && !plan->items[pj].full;
+    // a bottom item counts as loaded only if it holds the whole bottom (Q30: a window-cut item
+    // holds a prefix and leaves the rest on demand)
+    bool p_bottom = pj >= 0 && !plan->items[pj].full && plan->items[pj].rows == I - l.I_top;
     bool p_full = pj >= 0 && plan->items[pj].full;
     int8_t c;
     if ((cached && (l.I_top == I || p_bottom)) || p_full) c = kAlpha;
@@ -434,7 +439,11 @@ void ControlPlane::commit(int layer, const int32_t* ids, int B, const Plan* plan
   }
   // 6. on-demand PCIe bytes
   for (size_t a = 0; a < out.A.size(); ++a) {
-    if (out.cls[a] == kBeta) out.pcie_ondemand += (uint64_t)(I - l.I_top) * (uint64_t)row_bytes;
+    if (out.cls[a] == kBeta) {
+      const int pj = out.plan_idx[a];
+      const int pre = pj >= 0 && !plan->items[pj].full ? plan->items[pj].rows : 0;   // Q30 prefix
+      out.pcie_ondemand += (uint64_t)(I - l.I_top - pre) * (uint64_t)row_bytes;
+    }
     else if (out.cls[a] == kGamma) out.pcie_ondemand += (uint64_t)I * (uint64_t)row_bytes;
   }
 }
@@ -446,9 +455,11 @@ void ControlPlane::make_plan(int j, const int32_t* ranking, Plan& out) const {
   out.ranking.assign(ranking, ranking + N);
   if (!cfg.prefetch) return;
   const LayerState& l = layers[j];
-  const int64_t cap_rows = (int64_t)U_b * I;
+  int64_t cap_rows = (int64_t)U_b * I;
   int ycap = cfg.y_cap.empty() ? N : cfg.y_cap[j];
-  if (l.Y >= 0 && solver_y_cap) ycap = std::min(ycap, l.Y);
+  const bool window = !cfg.pf_rows.empty();   // Q30: the window replaces Alg. 1's count cap
+  if (window) cap_rows = std::min(cap_rows, cfg.pf_rows[j]);
+  else if (l.Y >= 0 && solver_y_cap) ycap = std::min(ycap, l.Y);
   int64_t used = 0;
   for (int y = 0; y < N; ++y) {
     int e = ranking[y];
@@ -464,7 +475,15 @@ void ControlPlane::make_plan(int j, const int32_t* ranking, Plan& out) const {
       it.rows = I;
       it.full = true;
     }
-    if (used + it.rows > cap_rows) break;
+    if (used + it.rows > cap_rows) {
+      const int64_t part = (int64_t)g * ((cap_rows - used) / g);
+      if (window && !it.full && part > 0) {   // Q30: the cut bottom keeps its prefix
+        it.rows = (int32_t)part;
+        it.buf_row = used;
+        out.items.push_back(it);
+      }
+      break;
+    }
     it.buf_row = used;
     used += it.rows;
     out.items.push_back(it);

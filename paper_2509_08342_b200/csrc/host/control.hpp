@@ -102,6 +102,7 @@ struct CacheParams {
   double zeta = 0.01;
   double t_att = 0, t_moe = 0, t_head = 0, t_load = 0;
   std::vector<int32_t> y_cap;         // empty -> N
+  std::vector<int64_t> pf_rows;       // reading Q30: per-layer prefetch window in rows (empty -> none)
   bool prefetch = true;
   uint64_t seed = 0;
 };

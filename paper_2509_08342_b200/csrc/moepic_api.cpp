@@ -162,6 +162,7 @@ CacheParams to_params(const moepic_cache_config* c, int L) {
   p.zeta = c->zeta;
   p.t_att = c->t_att; p.t_moe = c->t_moe; p.t_head = c->t_head; p.t_load = c->t_load_exp;
   if (c->y_cap_i) p.y_cap.assign(c->y_cap_i, c->y_cap_i + L);
+  if (c->prefetch_rows_i) p.pf_rows.assign(c->prefetch_rows_i, c->prefetch_rows_i + L);
   p.prefetch = c->prefetch != 0;
   p.seed = c->seed;
   return p;
@@ -1355,8 +1356,11 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   // K2 launch over everything but the tail runs while the tail is in flight.
   int n_copies = 0;
   for (size_t a = 0; a < res.A.size(); ++a) {
-    if (res.plan_idx[a] >= 0) continue;
     const int c = res.cls[a];
+    if (res.plan_idx[a] >= 0) {   // a window-cut bottom prefix (Q30): the rest loads on demand
+      if (c == kBeta) ++n_copies;
+      continue;
+    }
     if (c == kBeta || (c == kGamma && l.I_top < d.I)) ++n_copies;
     if (c == kGamma && l.I_top > 0) ++n_copies;
   }
@@ -1409,6 +1413,14 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     if (pj >= 0) {
       const PlanItem& it = used.items[pj];
       gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m, it.full ? 0 : l.I_top});
+      if (c == kBeta) {   // window-cut bottom (Q30): rows [I_top + prefix, I) on demand
+        const int r0 = l.I_top + it.rows, rows = d.I - r0;
+        uint8_t* dst = ctx->od_ptr(buf, od_row);
+        if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+        if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)r0 * rb, rows)) != MOEPIC_OK) return st;
+        gC.push_back(StepSeg{dst, e, rows, m, r0});
+        od_row += rows;
+      }
     } else if (c == kBeta || (c == kGamma && l.I_top < d.I)) {
       // missing bottom rows [I_top, I): known from classification alone (a gamma expert's top
       // rows follow in pass 2, once admission has chosen their destination)

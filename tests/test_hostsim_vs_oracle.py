@@ -118,12 +118,15 @@ if given is not None:
     @given(L=st.integers(1, 4), N=st.sampled_from([4, 8, 16, 32]), kfrac=st.floats(0.05, 0.6),
            I=st.sampled_from([64, 128, 256]), B=st.integers(1, 4), policy=st.sampled_from([P.LCP, P.LRU, P.LFU, P.RND]),
            prefetch=st.booleans(), vfrac=st.floats(0.0, 1.0), theta=st.sampled_from([None, 0.25, 0.5, 0.75, 1.0]),
-           ub_extra=st.integers(0, 2), n_shared=st.integers(0, 2), solver=st.booleans(), seed=st.integers(0, 10 ** 6))
+           ub_extra=st.integers(0, 2), n_shared=st.integers(0, 2), solver=st.booleans(), seed=st.integers(0, 10 ** 6),
+           window=st.sampled_from([None, 0, 16, 80, 300]))
     def test_random_configurations(L, N, kfrac, I, B, policy, prefetch, vfrac, theta, ub_extra, n_shared, solver,
-                                   seed):
+                                   seed, window):
         K = max(1, min(N - 1, int(round(kfrac * N))))
         v_e = round(vfrac * L * N, 2)
         kw = dict(v_e=v_e, policy=policy, prefetch=prefetch, seed=seed % 97)
+        if window is not None:
+            kw["prefetch_rows_i"] = [window] * L
         if theta is not None:
             kw["theta_i"] = [theta] * L
         skw = dict(use_solver=True, t_att=15.0, t_moe=30.0, t_head=5.0, t_load_exp=45.0, zeta=0.05)
@@ -171,3 +174,12 @@ def test_stats_checkpoint_round_trip():
         other.set_stats(blob)
     with pytest.raises(api.MoEpicError):
         b.set_stats(blob[:-8])
+
+
+@pytest.mark.parametrize("W", [0, 16, 48, 200])
+def test_window_plan_bit_exact(W):
+    """Reading Q30: the window-capped plan (cut bottoms keep their prefix) -- C++ control plane
+    equals the oracle, including with an Alg. 1 reconfiguration (the window then replaces Y)."""
+    _run_pair(3, 16, 4, 64, 128, 16, 4, 2, dict(v_e=6.0, prefetch_rows_i=[W] * 3, seed=5), T=60, seed=8)
+    kw = dict(v_e=10.0, t_att=20.0, t_moe=40.0, t_head=10.0, t_load_exp=35.0, zeta=0.02, prefetch_rows_i=[W] * 4)
+    _run_pair(4, 16, 2, 64, 128, 16, 2, 1, kw, T=80, seed=6, solver_at=40, solver_kw=dict(use_solver=True))

@@ -431,3 +431,60 @@ def test_pcie_bytes_closed_form_half_budget():
     for _ in range(20):
         tr = e.step(0, rng.choice(N, size=K, replace=False)[None])
         assert tr.pcie_ondemand == 352321536
+
+
+# ----------------------------------------------------------------- window-capped plan (Q30)
+def test_window_plan_vectors():
+    """Reading Q30 worked vectors (N = 10, K = 2, I = 128, g = 16, U_b = 2; expert 7's top cached
+    at theta = .5 -> its bottom is 64 rows; ranking 7, 3, 9, ...):
+      W = 200: 7 bottom (64) + 3 full (128) = 192; 9 full does not fit, full items are not cut
+      W = 100: 7 bottom (64); 3 full does not fit -> stop
+      W = 40 : 7 bottom cut to 16 * floor(40 / 16) = 32 rows
+      W = 8  : less than one granule -> empty plan
+    With W = 40 and 7 activated: beta, on-demand = (64 - 32) rows (Q30)."""
+    rank = np.array([7, 3, 9, 0, 1, 2, 4, 5, 6, 8])
+    expect = {200: [(7, False, 64), (3, True, 128)], 100: [(7, False, 64)], 40: [(7, False, 32)], 8: []}
+    for W, items in expect.items():
+        e = _engine(N=10, K=2, I=128, Ub=2)
+        e.configure(CacheConfig(v_e=0.5, theta_i=[0.5], prefetch_rows_i=[W]))   # C = 1 -> {0}
+        e.cache[0] = {7}
+        e.predict_prefetch(0, rank)
+        assert e.pending.items == items, (W, e.pending.items)
+    tr = e.step(0, np.array([[7, 1]]))                          # the W = 8 engine: nothing planned
+    assert dict(tr.act)[7] == BETA and tr.pcie_ondemand == (64 + 128) * 6 * 64
+    e = _engine(N=10, K=2, I=128, Ub=2)
+    e.configure(CacheConfig(v_e=0.5, theta_i=[0.5], prefetch_rows_i=[40]))
+    e.cache[0] = {7}
+    e.predict_prefetch(0, rank)
+    tr = e.step(0, np.array([[7, 1]]))
+    assert dict(tr.act) == {7: BETA, 1: GAMMA}
+    assert tr.pcie_ondemand == ((64 - 32) + 128) * 6 * 64
+    # a whole bottom inside the window is alpha, as without a window
+    e = _engine(N=10, K=2, I=128, Ub=2)
+    e.configure(CacheConfig(v_e=0.5, theta_i=[0.5], prefetch_rows_i=[100]))
+    e.cache[0] = {7}
+    e.predict_prefetch(0, rank)
+    assert dict(e.step(0, np.array([[7, 1]])).act)[7] == ALPHA
+
+
+def test_window_rows_cross_pcie_once():
+    """Conservation (any window, any policy): every non-resident row of an activated expert
+    crosses PCIe exactly once -- on-demand bytes + the prefetched rows of activated experts
+    = sum over A of (I - I_top if the top was cached else I) rows; and the plan never exceeds
+    min(U_b I, W) rows."""
+    rng = np.random.default_rng(17)
+    N, K, I, g = 12, 3, 128, 16
+    for W in (0, 16, 40, 100, 200, 1000):
+        e = OracleEngine(2, N, K, 64, I, row_granule=g, buffer_experts=K)
+        e.configure(CacheConfig(v_e=4.0, theta_i=[0.5, 0.75], prefetch_rows_i=[W, W], seed=3))
+        for t in range(60):
+            for i in range(2):
+                ids = rng.choice(N, size=K, replace=False)[None]
+                plan = e.pending if e.pending is not None and e.pending.target == i else None
+                cached_before = set(e.cache[i]) if e.cache_on(i) else set()
+                planned = {x: (f, r) for (x, f, r) in plan.items} if plan else {}
+                tr = e.step(i, ids, (i + 1) % 2, rng.permutation(N))
+                assert sum(r for (_, _, r) in e.pending.items) <= min(K * I, W)
+                need = sum((I - e.I_top[i]) if x in cached_before else I for (x, _) in tr.act)
+                pre = sum(planned[x][1] for (x, c) in tr.act if x in planned and c != GAMMA)
+                assert tr.pcie_ondemand == (need - pre) * 6 * 64, (W, t, i)
