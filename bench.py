@@ -237,6 +237,11 @@ def run_ours(args, log):
     t0 = time.time()
     y_cap = S.K * B if args.y_cap is None else args.y_cap
     base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[y_cap] * L, seed=0)
+    window_rows = None
+    if args.prefetch_window_us > 0:   # reading Q30: the link-idle window per layer, in expert rows
+        rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
+        window_rows = int(args.prefetch_window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
+        base_cfg["prefetch_rows_i"] = [window_rows] * L
     mode = MODES[args.mode]
     if "theta" in mode:
         base_cfg["theta_i"] = [mode["theta"]] * L
@@ -491,7 +496,8 @@ def run_ours(args, log):
                    "alg1": None if solved is None else dict(alg1_in, tau_tokens=args.tau,
                                                              theta_eff_i=[round(x, 4) for x in solved["theta_eff_i"]],
                                                              C_i=solved["C_i"]),
-                   "y_cap": y_cap,
+                   "y_cap": y_cap, "prefetch_window": None if window_rows is None else
+                   {"us": args.prefetch_window_us, "rows": window_rows},
                    "build_id": _build.build_id(),
                    "l2": "inputs larger than L2 (>=700 MB of expert rows streamed per layer)"},
         "layer_latency_us": {"mean": round(layer_us, 2),
@@ -693,6 +699,9 @@ def main():
     ap.add_argument("--alg1-inputs", default="model", choices=["model", "measured"],
                     help="Alg. 1 profile: fixed model of the box (reproducible, default) or this run's timings")
     ap.add_argument("--y-cap", type=int, default=None, help="prefetch count cap per layer (default K*B)")
+    ap.add_argument("--prefetch-window-us", type=float, default=0.0,
+                    help="reading Q30: cut each layer's prefetch plan at this many microseconds of link time "
+                         "(0 = no window: Alg. 1's Y caps the plan)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.e2e_steps is None:

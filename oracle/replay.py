@@ -23,10 +23,12 @@ Per step, in order:
      U_b * I rows or when the count reaches the Y cap.
      Reading Q30 (window-capped plan): with a per-layer prefetch window W_j in rows
      (prefetch_rows_i), the plan is cut at min(U_b * I, W_j) rows; the count cap is then
-     y_cap only (Alg. 1's Y stays inside the solver).  The item at the cut, if it is a
-     bottom, keeps its first g * floor(remaining / g) rows: "the router terminates the
-     prefetch" mid-item, deterministically at W_j.  An activated expert whose bottom
-     prefix was prefetched is beta (not fully resident) and loads only the rest.
+     y_cap only (Alg. 1's Y stays inside the solver).  The item at the cut (bottom or full
+     expert) keeps its first g * floor(remaining / g) rows: "the router terminates the
+     prefetch" mid-item, deterministically at W_j.  An activated expert with a
+     prefetched prefix is not fully resident: beta (bottom prefix) or gamma (prefix of
+     a full expert), and loads only the rest; an admitted gamma-with-prefix fills its slot
+     on the device (D2D of its top rows, as for a fully prefetched expert).
 """
 from __future__ import annotations
 
@@ -213,8 +215,8 @@ class OracleEngine:
                 rows, full = self.I, True
             if used + rows > cap_rows:
                 part = self.g * ((cap_rows - used) // self.g)
-                if window and not full and part > 0:      # Q30: the cut bottom keeps its prefix
-                    items.append((e, False, part))
+                if window and part > 0:                   # Q30: the cut item keeps its prefix
+                    items.append((e, full, part))
                 break
             items.append((e, full, rows))
             used += rows
@@ -254,7 +256,8 @@ class OracleEngine:
             cached = on and e in self.cache[i]
             p = planned.get(e)
             whole_bottom = p is not None and not p[0] and p[1] == I - self.I_top[i]
-            if (cached and (self.I_top[i] == I or whole_bottom)) or (p is not None and p[0]):
+            whole_expert = p is not None and p[0] and p[1] == I
+            if (cached and (self.I_top[i] == I or whole_bottom)) or whole_expert:
                 c = ALPHA
             elif cached:
                 c = BETA
@@ -296,7 +299,8 @@ class OracleEngine:
                     self.cache[i].remove(victim)
                     self.cache[i].add(e)
                     tr.adm.append((e, victim))
-                if cls[e] == ALPHA:       # full expert arrived by prefetch: D2D its top rows
+                if cls[e] == ALPHA or (e in planned and planned[e][0]):
+                    # full expert (or its prefix, Q30) arrived by prefetch: D2D its top rows
                     d2d += 2 * self.I_top[i] * self.row_bytes
         # 6. bytes
         rb = self.row_bytes
@@ -304,8 +308,9 @@ class OracleEngine:
             if cls[e] == BETA:   # minus a prefetched bottom prefix (Q30)
                 pre = planned[e][1] if e in planned and not planned[e][0] else 0
                 tr.pcie_ondemand += (I - self.I_top[i] - pre) * rb
-            elif cls[e] == GAMMA:
-                tr.pcie_ondemand += I * rb
+            elif cls[e] == GAMMA:   # minus a prefetched prefix of the full expert (Q30)
+                pre = planned[e][1] if e in planned and planned[e][0] else 0
+                tr.pcie_ondemand += (I - pre) * rb
         # 7. plan next layer
         n_router = 1
         if next_layer is not None and ranking_next is not None:

@@ -355,7 +355,7 @@ void ControlPlane::classify(int layer, const int32_t* ids, int B, const Plan* pl
     // a bottom item counts as loaded only if it holds the whole bottom (Q30: a window-cut item
     // holds a prefix and leaves the rest on demand)
     bool p_bottom = pj >= 0 && !plan->items[pj].full && plan->items[pj].rows == I - l.I_top;
-    bool p_full = pj >= 0 && plan->items[pj].full;
+    bool p_full = pj >= 0 && plan->items[pj].full && plan->items[pj].rows == I;
     int8_t c;
     if ((cached && (l.I_top == I || p_bottom)) || p_full) c = kAlpha;
     else if (cached) c = kBeta;
@@ -432,7 +432,8 @@ void ControlPlane::commit(int layer, const int32_t* ids, int B, const Plan* plan
         l.slot_expert[ad.slot] = e;
         l.slot_of[e] = ad.slot;
       }
-      ad.d2d_from_plan = out.cls[a] == kAlpha;   // full expert arrived by prefetch
+      // full expert (or its prefix, Q30) arrived by prefetch: its top rows are copied on the device
+      ad.d2d_from_plan = out.cls[a] == kAlpha || (out.plan_idx[a] >= 0 && plan->items[out.plan_idx[a]].full);
       if (ad.d2d_from_plan) out.d2d_bytes += 2ull * (uint64_t)l.I_top * (uint64_t)row_bytes;
       out.adm.push_back(ad);
     }
@@ -444,7 +445,11 @@ void ControlPlane::commit(int layer, const int32_t* ids, int B, const Plan* plan
       const int pre = pj >= 0 && !plan->items[pj].full ? plan->items[pj].rows : 0;   // Q30 prefix
       out.pcie_ondemand += (uint64_t)(I - l.I_top - pre) * (uint64_t)row_bytes;
     }
-    else if (out.cls[a] == kGamma) out.pcie_ondemand += (uint64_t)I * (uint64_t)row_bytes;
+    else if (out.cls[a] == kGamma) {
+      const int pj = out.plan_idx[a];
+      const int pre = pj >= 0 && plan->items[pj].full ? plan->items[pj].rows : 0;   // Q30 prefix
+      out.pcie_ondemand += (uint64_t)(I - pre) * (uint64_t)row_bytes;
+    }
   }
 }
 
@@ -477,7 +482,7 @@ void ControlPlane::make_plan(int j, const int32_t* ranking, Plan& out) const {
     }
     if (used + it.rows > cap_rows) {
       const int64_t part = (int64_t)g * ((cap_rows - used) / g);
-      if (window && !it.full && part > 0) {   // Q30: the cut bottom keeps its prefix
+      if (window && part > 0) {   // Q30: the cut item keeps its prefix
         it.rows = (int32_t)part;
         it.buf_row = used;
         out.items.push_back(it);

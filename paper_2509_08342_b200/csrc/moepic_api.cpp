@@ -1357,8 +1357,8 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   int n_copies = 0;
   for (size_t a = 0; a < res.A.size(); ++a) {
     const int c = res.cls[a];
-    if (res.plan_idx[a] >= 0) {   // a window-cut bottom prefix (Q30): the rest loads on demand
-      if (c == kBeta) ++n_copies;
+    if (res.plan_idx[a] >= 0) {   // a window-cut prefix (Q30): the rest loads on demand
+      if (c == kBeta || c == kGamma) ++n_copies;
       continue;
     }
     if (c == kBeta || (c == kGamma && l.I_top < d.I)) ++n_copies;
@@ -1403,6 +1403,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
       if (hi > lo) gA.push_back(StepSeg{ctx->shared_ptr(layer, s2) + lo * rb, -1 - s2, (int32_t)(hi - lo), all_tok, (int32_t)lo});
   }
   std::vector<uint32_t> masks(res.A.size());
+  std::vector<uint8_t*> od_rest(d.N, nullptr);   // gamma with a prefetched prefix: where row `prefix` lands
   for (size_t a = 0; a < res.A.size(); ++a) {   // pass 1: everything classification decides
     const int e = res.A[a];
     const uint32_t m = masks[a] = mask_of(e);
@@ -1413,8 +1414,9 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     if (pj >= 0) {
       const PlanItem& it = used.items[pj];
       gB.push_back(StepSeg{ctx->plan_ptr(buf, it.buf_row), e, it.rows, m, it.full ? 0 : l.I_top});
-      if (c == kBeta) {   // window-cut bottom (Q30): rows [I_top + prefix, I) on demand
-        const int r0 = l.I_top + it.rows, rows = d.I - r0;
+      if (c == kBeta || c == kGamma) {   // window-cut prefix (Q30): the rest of the rows on demand
+        const int r0 = (it.full ? 0 : l.I_top) + it.rows, rows = d.I - r0;
+        if (c == kGamma) od_rest[e] = ctx->od_ptr(buf, od_row);
         uint8_t* dst = ctx->od_ptr(buf, od_row);
         if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
         if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)r0 * rb, rows)) != MOEPIC_OK) return st;
@@ -1549,13 +1551,20 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   ++launches;
   }
   }
-  // alpha experts that arrived as full prefetches and were admitted: D2D their top rows
+  // admitted experts that arrived as full prefetches (or a prefix of one, Q30): D2D their top
+  // rows -- from the plan buffer, and past the prefix from the on-demand region
   for (const auto& a : res.adm) {
     if (!a.d2d_from_plan || a.victim == kAdmNone || l.I_top == 0) continue;
     const int pj = [&] { for (size_t k = 0; k < used.items.size(); ++k) if (used.items[k].expert == a.expert) return (int)k; return -1; }();
     if (pj < 0) continue;
+    const int pre = std::min(used.items[pj].rows, l.I_top);
     CK(cudaMemcpyAsync(ctx->slot_ptr(layer, a.slot), ctx->plan_ptr(buf, used.items[pj].buf_row),
-                       (size_t)l.I_top * rb, cudaMemcpyDeviceToDevice, s));
+                       (size_t)pre * rb, cudaMemcpyDeviceToDevice, s));
+    if (pre < l.I_top) {
+      if (!od_rest[a.expert]) return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: prefix rest not on demand");
+      CK(cudaMemcpyAsync(ctx->slot_ptr(layer, a.slot) + (size_t)pre * rb, od_rest[a.expert],
+                         (size_t)(l.I_top - pre) * rb, cudaMemcpyDeviceToDevice, s));
+    }
   }
   if (ctx->poison) {   // this step's half and partials are dead once its kernels are done
     CK(cudaMemsetAsync(ctx->arena + ctx->lay.buf[buf], 0xFF, (ctx->lay.plan_rows + ctx->lay.od_rows) * rb, s));

@@ -104,7 +104,7 @@ def router_weights(seed: int, layer: int, N: int, d: int, kappa: float = 0.5) ->
 def hidden_states(seed: int, T: int, L: int, d: int, mu: float = 1.0, a: float = 0.35,
                   eps: float = 0.35, scale: float = 1.0) -> torch.Tensor:
     """h[t][i] bf16 [T][L][d]: AR(1) token process + per-layer perturbation."""
-    g = _gen(seed, 4, T, L)
+    g = _gen(seed, 4, L)   # prefix-stable: the first t tokens do not depend on T
     u = _unit_u(seed, d)
     x = torch.randn(d, generator=g, dtype=torch.float64)
     out = torch.empty(T, L, d, dtype=torch.float64)

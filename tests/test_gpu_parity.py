@@ -345,17 +345,19 @@ def test_cancel_prefetch_same_results_fewer_bytes():
     assert c_on["pcie_prefetch_bytes"] < c_on["pcie_prefetch_planned_bytes"]
 
 
-@pytest.mark.parametrize("B,W", [(1, 64), (1, 192), (3, 128), (40, 192)])
-def test_window_cut_prefetch(B, W):
-    """Reading Q30 on the GPU: plans cut at W rows; a cut bottom's prefix is computed from the
-    plan buffer (after the plan event) and the rest of it from the on-demand region -- two
-    segments of one expert, on K2 (B <= 32) and on the tcgen05 prefill path (B = 40).  Traces
-    and bytes bit-exact, y within 2e-3 (split identity)."""
+@pytest.mark.parametrize("B,W,th", [(1, 64, 0.5), (1, 192, 0.5), (3, 128, 0.5), (40, 192, 0.5), (1, 320, 1.0),
+                                    (2, 128, 1.0), (40, 448, 1.0)])
+def test_window_cut_prefetch(B, W, th):
+    """Reading Q30 on the GPU: plans cut at W rows; a cut item's prefix (of a bottom, or of a
+    full expert) is computed from the plan buffer (after the plan event) and the rest of it
+    from the on-demand region -- two segments of one expert, on K2 (B <= 32) and on the tcgen05
+    prefill path (B = 40); an admitted gamma with a prefix fills its slot by D2D from both.
+    Traces and bytes bit-exact, y within 2e-3 (split identity)."""
     api = _api()
     m = Model(3, 8, 2, 256, 512, seed=29)
     ctx = _ctx(m, max_batch=B, v_e_max=12.0, g=64)
     orc = OracleEngine(3, 8, 2, 256, 512, row_granule=64)
-    cfg = dict(v_e=6.0, theta_i=[0.5, 0.25, 0.5], prefetch_rows_i=[W] * 3, seed=2)
+    cfg = dict(v_e=6.0 if th < 1 else 3.0, theta_i=[th, th / 2, th], prefetch_rows_i=[W] * 3, seed=2)
     ctx.configure(**cfg)
     orc.configure(CacheConfig(**cfg))
     H = synth.hidden_states(41, 4 * B, 3, 256)

@@ -437,13 +437,14 @@ def test_pcie_bytes_closed_form_half_budget():
 def test_window_plan_vectors():
     """Reading Q30 worked vectors (N = 10, K = 2, I = 128, g = 16, U_b = 2; expert 7's top cached
     at theta = .5 -> its bottom is 64 rows; ranking 7, 3, 9, ...):
-      W = 200: 7 bottom (64) + 3 full (128) = 192; 9 full does not fit, full items are not cut
-      W = 100: 7 bottom (64); 3 full does not fit -> stop
+      W = 200: 7 bottom (64) + 3 full (128) = 192; 8 rows left, less than one granule
+      W = 100: 7 bottom (64) + 3 full cut to 16 * floor(36 / 16) = 32 rows
       W = 40 : 7 bottom cut to 16 * floor(40 / 16) = 32 rows
       W = 8  : less than one granule -> empty plan
     With W = 40 and 7 activated: beta, on-demand = (64 - 32) rows (Q30)."""
     rank = np.array([7, 3, 9, 0, 1, 2, 4, 5, 6, 8])
-    expect = {200: [(7, False, 64), (3, True, 128)], 100: [(7, False, 64)], 40: [(7, False, 32)], 8: []}
+    expect = {200: [(7, False, 64), (3, True, 128)], 100: [(7, False, 64), (3, True, 32)], 40: [(7, False, 32)],
+              8: []}
     for W, items in expect.items():
         e = _engine(N=10, K=2, I=128, Ub=2)
         e.configure(CacheConfig(v_e=0.5, theta_i=[0.5], prefetch_rows_i=[W]))   # C = 1 -> {0}
@@ -459,12 +460,16 @@ def test_window_plan_vectors():
     tr = e.step(0, np.array([[7, 1]]))
     assert dict(tr.act) == {7: BETA, 1: GAMMA}
     assert tr.pcie_ondemand == ((64 - 32) + 128) * 6 * 64
-    # a whole bottom inside the window is alpha, as without a window
+    # a whole bottom inside the window is alpha, as without a window; expert 3 with a 32-row
+    # prefix of the full expert is gamma, loads 96 rows, is admitted (victim 0 -- 7 is in A)
+    # and fills its slot's top rows on the device: d2d = 2 * I_top rows
     e = _engine(N=10, K=2, I=128, Ub=2)
-    e.configure(CacheConfig(v_e=0.5, theta_i=[0.5], prefetch_rows_i=[100]))
-    e.cache[0] = {7}
+    e.configure(CacheConfig(v_e=1.0, theta_i=[0.5], prefetch_rows_i=[100]))   # C = 2 -> {0, 1}
+    e.cache[0] = {7, 0}
     e.predict_prefetch(0, rank)
-    assert dict(e.step(0, np.array([[7, 1]])).act)[7] == ALPHA
+    tr = e.step(0, np.array([[7, 3]]))
+    assert dict(tr.act) == {7: ALPHA, 3: GAMMA} and tr.adm == [(3, 0)]
+    assert tr.pcie_ondemand == (128 - 32) * 6 * 64
 
 
 def test_window_rows_cross_pcie_once():
@@ -486,5 +491,5 @@ def test_window_rows_cross_pcie_once():
                 tr = e.step(i, ids, (i + 1) % 2, rng.permutation(N))
                 assert sum(r for (_, _, r) in e.pending.items) <= min(K * I, W)
                 need = sum((I - e.I_top[i]) if x in cached_before else I for (x, _) in tr.act)
-                pre = sum(planned[x][1] for (x, c) in tr.act if x in planned and c != GAMMA)
+                pre = sum(planned[x][1] for (x, c) in tr.act if x in planned)
                 assert tr.pcie_ondemand == (need - pre) * 6 * 64, (W, t, i)
