@@ -22,7 +22,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/combine.cu", "kernels/prefill.cu",
+CU_SOURCES = ["kernels/router.cu", "kernels/expert.cu", "kernels/expert_tc.cu", "kernels/combine.cu", "kernels/prefill.cu",
               "kernels/attention.cu", "kernels/ep.cu"]
 CXX_SOURCES = ["host/control.cpp", "host/ep_plan.cpp", "moepic_api.cpp"]
 

@@ -561,6 +561,7 @@ bool kernels_init(char* err, size_t errlen) {
 #undef MOEPIC_ATTR
   if ((r = router_init()) != cudaSuccess) e = r;
   if ((r = combine_init()) != cudaSuccess) e = r;
+  if ((r = k2t_init()) != cudaSuccess) e = r;
   if ((r = attention_init()) != cudaSuccess) e = r;
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));

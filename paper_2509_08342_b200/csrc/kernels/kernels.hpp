@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #ifdef __CUDACC__
@@ -95,6 +96,35 @@ int k2_rows_per_tile(int d, int q4);
 int k2_max_tokens(int d, int q4);
 size_t k2_smem_bytes(int d, int q4);
 void launch_k2(const K2Params& p, int grid, int tb, cudaStream_t s);
+
+// ------------------------------------------------------------------ K2T: tcgen05 decode (B_e > 4)
+// Segments of 64-row units read through one tensor map over the arena's row region; the launch
+// writes one partial [G][B][d] (combined by K3 like any (segment, CTA) partial with tok_mask
+// (1 << B) - 1 and nchunks = G).  Needs bf16 rows, d % 256 == 0, d <= 2048, B <= 16.
+struct K2TSeg {
+  int64_t map_row;        // tensor-map row of the segment's first row
+  int32_t unit_begin;     // first 64-row unit of the segment in this launch
+  int32_t expert;         // routed expert id, or -1 - s for shared expert s (weight 1)
+  uint32_t tok_mask;      // tokens this segment serves
+  int32_t pad;
+};
+struct K2TParams {
+  const CUtensorMap* tmW;
+  CUtensorMap tmH;
+  const int32_t* ids;
+  const float* w;
+  float* ws;              // this launch's partial area [G][B][d]
+  int d, K, B, nsegs, units;
+  int mode;               // MOEPIC_K2T_MODE diagnostics: 1 = no MMAs (operand streaming only)
+  unsigned long long* tstamp;
+  unsigned long long* dbg;          // MOEPIC_K2_TRACE per-CTA stamps [G][8] (tools) or nullptr
+  K2TSeg segs[kMaxLaunchSegs];
+};
+constexpr int kK2TMaxB = 16;
+constexpr int kK2TMaxD = 2048;
+void launch_k2t(const K2TParams& p, int grid, cudaStream_t s);
+size_t k2t_smem_bytes(int d);
+cudaError_t k2t_init();
 
 // ------------------------------------------------------------------ K3: combine
 struct CombineParams {

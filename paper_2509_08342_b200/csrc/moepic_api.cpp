@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <numeric>
 #include <new>
 #include <string>
 #include <vector>
@@ -42,7 +43,7 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 
 struct ArenaLayout {
   size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, hstage, ystage, total;
-  uint64_t pool_rows, plan_rows, od_rows, ws_floats;
+  uint64_t pool_rows, plan_rows, od_rows, ws_floats, map_rows;
   // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
   size_t xperm, aact, yperm, pos, cursor;
   uint64_t pf_rows;
@@ -50,6 +51,14 @@ struct ArenaLayout {
 constexpr int kDecodeMaxB = 32;   // decode path (K2) serves up to 32 tokens (token bit masks)
 
 int n_local(const moepic_model_desc& d) { return d.N / d.ep_size; }
+
+// K2T (kernels/expert_tc.cu) serves decode steps whose experts take more tokens than K2's token
+// block: bf16 rows, d a multiple of 256 up to 2048 (TMEM holds the [d][16] accumulator), 64-row
+// units (row granule), batches of 5..16 tokens.  MOEPIC_K2T=0 at create keeps every step on K2.
+bool k2t_eligible(const moepic_model_desc& d) {
+  return d.weight_format == MOEPIC_BF16 && d.d % 256 == 0 && d.d <= kK2TMaxD &&
+         d.row_granule % 64 == 0 && d.max_batch > 4;
+}
 
 std::string validate_desc(const moepic_model_desc* d) {
   if (!d) return "desc is NULL";
@@ -106,14 +115,26 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   const int Nl = n_local(d);
   size_t off = 0;
   a.routers = off; off = align_up(off + (size_t)d.L * d.N * d.d * 2);
+  // shared experts, slot pool and ping-pong buffers are one row region: every region starts a
+  // whole number of rows after a.shared, so one 3-D tensor map {d, 3, rows} over it addresses
+  // any segment by its row index (K2T)
   a.shared = off; off = align_up(off + (size_t)d.L * d.n_shared * d.I * rb);
+  const size_t rowal = std::lcm((size_t)rb, kAlign);
+  auto row_align = [&](size_t x) { return a.shared + align_up(x - a.shared, rowal); };
   a.pool_rows = (uint64_t)std::ceil(d.v_e_max * (double)d.I - 1e-9);
+  off = row_align(off);
   a.pool = off; off = align_up(off + a.pool_rows * rb);
   a.plan_rows = (uint64_t)d.buffer_experts * d.I;
   a.od_rows = (uint64_t)std::min(Nl, d.max_batch * d.K) * d.I;
-  for (int i = 0; i < 2; ++i) { a.buf[i] = off; off = align_up(off + (a.plan_rows + a.od_rows) * rb); }
+  for (int i = 0; i < 2; ++i) {
+    off = row_align(off);
+    a.buf[i] = off; off = align_up(off + (a.plan_rows + a.od_rows) * rb);
+  }
+  a.map_rows = (a.buf[1] - a.shared) / rb + a.plan_rows + a.od_rows;
   const uint64_t Bd = (uint64_t)std::min(d.max_batch, kDecodeMaxB);
   a.ws_floats = (uint64_t)d.d * (4ull * (Bd * d.K + d.n_shared * Bd) + 3ull * (kSMs + 1) * 8 + 64);
+  if (k2t_eligible(d))   // K2T partials: one [G][B][d] area per launch, up to 3 launches per step
+    a.ws_floats += 3ull * kSMs * std::min<uint64_t>(Bd, kK2TMaxB) * d.d;
   a.ws = off; off = align_up(off + a.ws_floats * 4);
   a.logits = off; off = align_up(off + (size_t)2 * d.max_batch * d.N * 8);
   a.ids = off; off = align_up(off + (size_t)d.max_batch * d.K * 4);
@@ -313,8 +334,13 @@ EpOffsets ep_offsets(int G, int T_max, int Bl_max, int B_dec, int K, int d) {
 
 // ====================================================================== context
 struct moepic_ctx {
+  // K2T: one tensor map over the arena's row region (shared experts | slot pool | buffers)
+  alignas(64) CUtensorMap tm_rows;
+  bool k2t = false;
+  int k2t_mode = 0;   // MOEPIC_K2T_MODE (tools): 1 = K2T streams its operands without MMAs
   // kernel parameter blocks (large: built here, not on the stack; calls on a ctx are serialised)
   std::unique_ptr<K2Params> kp = std::make_unique<K2Params>();
+  std::unique_ptr<K2TParams> ktp = std::make_unique<K2TParams>();
   std::unique_ptr<PfPermuteParams> pf_pp = std::make_unique<PfPermuteParams>();
   std::unique_ptr<PfGemmParams> pf_gp = std::make_unique<PfGemmParams>();
   std::unique_ptr<CombineParams> cpar = std::make_unique<CombineParams>();
@@ -557,6 +583,11 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->scratch_d), ctx->scratch_h, 0) != cudaSuccess)
     return bail(MOEPIC_ENOMEM);
   if (desc->max_batch > kDecodeMaxB && !prefill_init(kerr, sizeof kerr)) return bail(MOEPIC_ERUNTIME);
+  if (k2t_eligible(*desc) && !(getenv("MOEPIC_K2T") && atoi(getenv("MOEPIC_K2T")) == 0)) {
+    if (!pf_tmap_weights(&ctx->tm_rows, ctx->arena + lay.shared, lay.map_rows, desc->d, 64))
+      return bail(MOEPIC_ERUNTIME);
+    ctx->k2t = true;
+  }
   const uint64_t host_bytes = (uint64_t)desc->L_host * ctx->Nl() * desc->I * ctx->rb();
   if (cudaHostAlloc(&ctx->host_experts, host_bytes, cudaHostAllocDefault) != cudaSuccess) {
     cudaGetLastError();
@@ -582,6 +613,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (const char* e = getenv("MOEPIC_OD_TAIL_KB")) ctx->od_tail_bytes = (size_t)atol(e) << 10;   // tests: small shapes
   if (const char* e = getenv("MOEPIC_FEED_DEPTH")) ctx->kFeedDepth = (size_t)std::min(atol(e), (long)moepic_ctx::kFeedRing);
   if (const char* e = getenv("MOEPIC_PF_CTA_PAIR")) ctx->pf_cta_pair = atoi(e) ? 1 : 0;
+  if (const char* e = getenv("MOEPIC_K2T_MODE")) ctx->k2t_mode = atoi(e);
   ctx->k1_trace = getenv("MOEPIC_K1_TRACE") != nullptr;
   ctx->k2_trace = getenv("MOEPIC_K2_TRACE") != nullptr;
   ctx->host_timing = getenv("MOEPIC_HOST_TIMING") != nullptr;
@@ -793,11 +825,100 @@ struct FuseCombine {
   bool done;
 };
 
+// K2T launches over a segment group (kernels/expert_tc.cu): every weight row is read once for the
+// whole batch; each launch leaves one [G][B][d] partial that K3 adds in its fixed order.
+static moepic_status launch_group_tc(moepic_ctx* ctx, const std::vector<StepSeg>& segs, const uint16_t* h, int B,
+                                     cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb,
+                                     int& launches) {
+  const int d = ctx->desc.d;
+  const uint8_t* rbase = ctx->arena + ctx->lay.shared;
+  K2TParams& kp = *ctx->ktp;
+  if (!pf_tmap_2d(&kp.tmH, h, (uint64_t)B, (uint64_t)d, kK2TMaxB))
+    return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (h)");
+  std::vector<const StepSeg*> work;
+  for (const auto& sg : segs)
+    if (sg.nrows > 0 && sg.mask != 0) work.push_back(&sg);
+  for (size_t i0 = 0; i0 < work.size(); i0 += kMaxLaunchSegs) {
+    const size_t i1 = std::min(work.size(), i0 + (size_t)kMaxLaunchSegs);
+    int units = 0;
+    uint64_t rows = 0;
+    for (size_t i = i0; i < i1; ++i) {
+      K2TSeg& g = kp.segs[i - i0];
+      g.map_row = (int64_t)((uint64_t)(work[i]->base - rbase) / ctx->rb());
+      g.unit_begin = units;
+      g.expert = work[i]->expert;
+      g.tok_mask = work[i]->mask;
+      g.pad = 0;
+      units += work[i]->nrows / 64;
+      rows += (uint64_t)work[i]->nrows;
+    }
+    const int G = std::min(kSMs, units);
+    if ((uint64_t)(ws_next + (int64_t)G * B * d) > ctx->lay.ws_floats)
+      return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "workspace overflow (%lld floats)", (long long)ws_next);
+    kp.tmW = &ctx->tm_rows;
+    kp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids);
+    kp.w = reinterpret_cast<const float*>(ctx->arena + ctx->lay.w);
+    kp.ws = reinterpret_cast<float*>(ctx->arena + ctx->lay.ws) + ws_next;
+    kp.d = d;
+    kp.K = ctx->desc.K;
+    kp.B = B;
+    kp.nsegs = (int)(i1 - i0);
+    kp.units = units;
+    kp.mode = ctx->k2t_mode;
+    comb.push_back(CombineSeg{ws_next, G, (uint32_t)((1ull << B) - 1)});
+    ws_next += (int64_t)G * B * d;
+    const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
+    kp.tstamp = ctx->tstamp(pe);
+    static unsigned long long* dbg_buf = nullptr;   // MOEPIC_K2_TRACE: per-CTA phases to stderr (tools)
+    kp.dbg = nullptr;
+    if (ctx->k2_trace) {
+      if (!dbg_buf) cudaMalloc(&dbg_buf, 148 * 8 * 8);
+      cudaMemsetAsync(dbg_buf, 0, 148 * 8 * 8, s);
+      kp.dbg = dbg_buf;
+    }
+    launch_k2t(kp, G, s);
+    if (ctx->k2_trace) {
+      unsigned long long hb[148 * 8];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(hb, dbg_buf, sizeof hb, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0}, mn[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+      double avg[4] = {0, 0, 0, 0};
+      for (int c = 0; c < G; ++c) t0 = std::min(t0, hb[c * 8]);
+      for (int c = 0; c < G; ++c) {
+        for (int k = 0; k < 4; ++k) {
+          const unsigned long long v = hb[c * 8 + k] - t0;
+          mx[k] = std::max(mx[k], v);
+          mn[k] = std::min(mn[k], v);
+          avg[k] += (double)(k == 2 ? hb[c * 8 + 6] & ((1ull << 40) - 1) : hb[c * 8 + 4 + k]) / G;
+        }
+      }
+      fprintf(stderr, "[k2ttrace] G=%d units=%d rows=%llu start %llu..%llu mma_done %llu..%llu flush %llu..%llu "
+              "end %llu..%llu ns | avg wait cycles: producer-empty %.0f mma-full %.0f mma-issue %.0f epi-gu %.0f\n",
+              G, units, (unsigned long long)rows, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], avg[0],
+              avg[1], avg[2], avg[3]);
+    }
+    ctx->prof_end(pe, s, rows * ctx->rb() + (uint64_t)B * d * 2);   // each weight row once
+    CK(cudaGetLastError());
+    ++launches;
+  }
+  return MOEPIC_OK;
+}
+
 static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& segs, const uint16_t* h, int B,
                                   cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb, int& launches,
                                   FuseCombine* fuse = nullptr) {
   const int d = ctx->desc.d;
   const int tbmax = k2_max_tokens(d, ctx->desc.weight_format == MOEPIC_Q4G64);
+  if (ctx->k2t && B <= kK2TMaxB) {   // an expert with more tokens than K2's block: K2T reads it once
+    bool hot = false, ok = true;
+    const uint8_t* rbase = ctx->arena + ctx->lay.shared;
+    for (const auto& sg : segs) {
+      if (sg.nrows <= 0 || sg.mask == 0) continue;
+      hot |= __builtin_popcount(sg.mask) > tbmax;
+      ok &= sg.nrows % 64 == 0 && sg.base >= rbase && (uint64_t)(sg.base - rbase) % ctx->rb() == 0;
+    }
+    if (hot && ok) return launch_group_tc(ctx, segs, h, B, s, ws_next, comb, launches);
+  }
   // split by token groups of <= tbmax tokens
   std::vector<StepSeg> work;
   for (const auto& sg : segs) {
