@@ -23,6 +23,22 @@ __device__ __forceinline__ void unpack4(const uint2& v, float* f) {
   f[2] = bf16lo(v.y); f[3] = bf16hi(v.y);
 }
 
+// fp16 pairs (the stored down columns, reading Q31) to fp32
+__device__ __forceinline__ float2 h2f2(uint32_t v) {
+  float2 r;
+  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ void unpack8_f16(const uint4& v, float* f) {
+  float2 a = h2f2(v.x), b = h2f2(v.y), c = h2f2(v.z), d = h2f2(v.w);
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y; f[4] = c.x; f[5] = c.y; f[6] = d.x; f[7] = d.y;
+}
+__device__ __forceinline__ void unpack4_f16(const uint2& v, float* f) {
+  float2 a = h2f2(v.x), b = h2f2(v.y);
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+
 // Blackwell paired fp32 FMA (SASS FFMA2): (d0, d1) += (a0 * b0, a1 * b1) in one instruction
 __device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
   asm("{\n\t.reg .b64 ra, rb, rc;\n\t"

@@ -1,7 +1,7 @@
 // K2 split-expert streaming SwiGLU for decode batches.
 //
 // A segment is a contiguous row range of one expert in the row-interleaved layout
-// [gate_r | up_r | down[:, r]] (6d bytes per row): a cached top (HBM slot), a prefetched or
+// [gate_r | up_r | down[:, r]] (6d bytes per row; gate / up bf16, down fp16, reading Q31): a cached top (HBM slot), a prefetched or
 // on-demand bottom (ping-pong buffer), a full expert, or a shared expert's rows.  The split-sum
 // identity (y = y_top + y_bottom) means a segment is just a base pointer and a row count.
 //
@@ -152,10 +152,15 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
 
   // the thread's CW weights of part (0 gate, 1 up, 2 down) of a stored row, as fp32
   auto load_part = [&](const uint8_t* row, int part, float* f) {
-    if constexpr (Q4 == 0) {
+    if constexpr (Q4 == 0) {   // gate / up bf16, down fp16 (reading Q31)
       const uint8_t* base = row + (size_t)part * 2 * d;
-      if constexpr (CW == 8) unpack8(*reinterpret_cast<const uint4*>(base + c0 * 2), f);
-      else unpack4(*reinterpret_cast<const uint2*>(base + c0 * 2), f);
+      if (part == 2) {
+        if constexpr (CW == 8) unpack8_f16(*reinterpret_cast<const uint4*>(base + c0 * 2), f);
+        else unpack4_f16(*reinterpret_cast<const uint2*>(base + c0 * 2), f);
+      } else {
+        if constexpr (CW == 8) unpack8(*reinterpret_cast<const uint4*>(base + c0 * 2), f);
+        else unpack4(*reinterpret_cast<const uint2*>(base + c0 * 2), f);
+      }
     } else {   // x = min + code * scale; code -> float exactly via the 2^23 magic constant
       const uint32_t prm =
           *reinterpret_cast<const uint32_t*>(row + 3 * (d / 2) + (part * (d >> 6) + (c0 >> 6)) * 4);

@@ -11,11 +11,11 @@
 //            UMMA M = 128 (rows), N = 16 (the whole batch, B <= 16, zero rows past B), K = d;
 //            A = weight tile (K-major, TMA 128-byte swizzle), B = h tile (K-major, TMA).
 //   epilogue a[r][t] = silu(g) * u * w_{t, e(r)} for t in the segment's token set, else 0
-//            (Eq. 2 weight folded in), split a = hi + lo (two bf16), written to
-//            shared memory as the K-major B operand of the down MMA.
+//            (Eq. 2 weight folded in), rounded to fp16 (the stored down columns are fp16,
+//            reading Q31) and written to shared memory as the K-major B operand of the down MMA.
 //   down     D2[mt] [128 cols][16 tokens] += Down[128 rows][cols mt]^T . a[128 rows][16]:
 //            UMMA M = 128 (output columns, MN-major A straight from the row-interleaved rows),
-//            N = 16, K = 128 rows, hi and lo MMAs.  D2 covers all d columns (d / 128 tiles of 16
+//            N = 16, K = 128 rows, fp16 x fp16.  D2 covers all d columns (d / 128 tiles of 16
 //            TMEM columns) and accumulates over EVERY block of the CTA, whatever the segment:
 //            the token weight is inside a, so D2[.][t] is this CTA's share of y[t].
 //   flush    D2 -> workspace partial [G][B][d] once per launch (combined in fixed order by K3).
@@ -43,15 +43,10 @@ namespace {
 constexpr int kTcThreads = 192;
 constexpr int kTcMaxStages = 6;
 constexpr uint32_t kTcStage = 32768;   // always 32 KB of weights (see the stage table above)
-constexpr uint32_t kTcB2 = 8192;       // a: [hi | lo] x [unit A | unit B] x 16 tokens x 64 rows
+constexpr uint32_t kTcB2 = 4096;       // a (fp16): [unit A | unit B] x 16 tokens x 64 rows
 constexpr uint32_t kTcSmemMax = 227 * 1024;
 constexpr uint32_t kTcTmemCols = 512;
 constexpr int kTcN = 16;
-
-__device__ __forceinline__ uint32_t bf16_rne_tc(float a) {
-  const uint32_t u = __float_as_uint(a);
-  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
-}
 
 // Segment of unit u by a forward-only cursor: each role visits its units in increasing order, so
 // the walk over the segment table (kernel parameters, constant cache) is amortised to O(1) per
@@ -196,7 +191,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k2t_split_expert(const __grid_c
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_gu = make_idesc(128, kTcN, 0, 0);   // A rows K-major, B h K-major
-      constexpr uint32_t idesc_dn = make_idesc(128, kTcN, 0, 1);   // A down columns MN-major
+      constexpr uint32_t idesc_dn = make_idesc(128, kTcN, 0, 1, 1);   // fp16: A down columns MN-major, B = a
       int it = 0;
       mbar_wait(h_full, 0);
       const uint32_t hb = smem_u32(hs);
@@ -252,8 +247,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k2t_split_expert(const __grid_c
               const uint64_t da = desc_mn_sw128(sa + sub * 16384 + kk * 2048, 8192, 1024);
               const uint32_t acc = (j == 0 && (sub == 0 || !hasB) && kk == 0) ? 0u : 1u;
               if (p.mode & 1) continue;
-              umma<1>(d2, da, desc_k_sw128(ab + bu + kk * 32), idesc_dn, acc);          // a_hi
-              umma<1>(d2, da, desc_k_sw128(ab + 4096 + bu + kk * 32), idesc_dn, 1u);    // + a_lo
+              umma<1>(d2, da, desc_k_sw128(ab + bu + kk * 32), idesc_dn, acc);
             }
           }
           umma_commit<1>(&empty[st]);
@@ -314,13 +308,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k2t_split_expert(const __grid_c
       for (int t = 0; t < 16; ++t) {
         const float wv = wt[buf * 32 + unit * 16 + t];
         const float a = (valid && wv != 0.f) ? g[t] / (1.f + __expf(-g[t])) * u[t] * wv : 0.f;
-        const uint32_t hi = bf16_rne_tc(a);
-        const uint32_t lo = bf16_rne_tc(a - __uint_as_float(hi << 16));
         // K-major 128-byte swizzle: token t = row (t & 7) of 8-row group t >> 3; 16-byte chunk
         // r64 / 8 stored at chunk (r64 / 8) ^ (t & 7)
         const uint32_t off = (uint32_t)((t >> 3) * 1024 + (t & 7) * 128 + ((((r64 >> 3) ^ (t & 7)) & 7) << 4) + (r64 & 7) * 2);
-        *reinterpret_cast<uint16_t*>(ab + off) = (uint16_t)hi;
-        *reinterpret_cast<uint16_t*>(ab + 4096 + off) = (uint16_t)lo;
+        *reinterpret_cast<uint16_t*>(ab + off) = (uint16_t)f16_sat(a);
       }
       fence_proxy_async_smem();
       tc_fence_before();

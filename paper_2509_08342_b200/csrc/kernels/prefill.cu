@@ -11,9 +11,10 @@
 //   warps 2-9 epilogue: tcgen05.ld 32 lanes x 16 columns, SwiGLU (gate/up) or fp32 store (down),
 //           then arrive on `tempty` so the MMA warp can reuse that accumulator.
 // gate/up: [D_g | D_u] = X_e [W_g; W_u]^T as one N = 256 MMA per K step;
-//          a = silu(D_g) * D_u -> bf16 A_act[rows][I] at the segment's intermediate columns.
+//          a = silu(D_g) * D_u -> fp16 A_act[rows][I] at the segment's intermediate columns.
 // down:    Y[rows][n0..n0+256) (+)= A_act[rows][seg] * Down[seg][n0..], the down rows are
-//          N-contiguous in the row-interleaved layout, so B is an MN-major operand.
+//          N-contiguous in the row-interleaved layout, so B is an MN-major operand; both are fp16
+//          (the stored down columns are fp16, reading Q31), one MMA per K step.
 // Weights are read through a 3-D tensor map {d, 3, rows} over the row-interleaved layout
 // [gate_r | up_r | down[:, r]] so the same rows serve both GEMMs without any repacking.
 #include "prefill.hpp"
@@ -35,13 +36,13 @@ constexpr uint32_t kAccCols = 256;             // one fp32 accumulator tile (N =
 constexpr uint32_t kTmemCols = 2 * kAccCols;   // double-buffered: epilogue of tile j || MMA of j+1
 constexpr uint32_t kABytes = kPfBM * kPfBK * 2;        // 16 KB
 // CG = 1 (one CTA, UMMA M = 128):  gate/up stage A | B_gate | B_up (48 KB) x 4,
-//                                   down stage A_hi | A_lo | B[256 cols] (64 KB) x 3.
+//                                   down stage A | B[256 cols] (48 KB) x 4.
 // CG = 2 (CTA pair, cta_group::2, UMMA M = 256, each CTA holds half of A and half of B):
 //                                   gate/up A | B_gate or B_up (32 KB) x 6,
-//                                   down A_hi | A_lo | B[128 cols] (48 KB) x 4.
+//                                   down A | B[128 cols] (32 KB) x 6.
 template <bool DOWN, int CG> struct Cfg {
   static constexpr uint32_t kBBytes = 32 * 1024 / CG;
-  static constexpr uint32_t kBOff = DOWN ? 2 * kABytes : kABytes;
+  static constexpr uint32_t kBOff = kABytes;
   static constexpr uint32_t kStageBytes = kBOff + kBBytes;
   static constexpr int kStages = (int)((192 * 1024) / kStageBytes);
 };
@@ -50,13 +51,6 @@ __device__ __forceinline__ uint32_t bf16_rne(float a) {   // round-to-nearest-ev
   const uint32_t u = __float_as_uint(a);
   return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
 }
-// a = hi + lo with hi = bf16(a), lo = bf16(a - hi): the down GEMM consumes both (2 MMAs), so the
-// intermediate activation carries ~16 mantissa bits instead of bf16's 8
-__device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) {
-  hi = bf16_rne(a);
-  lo = bf16_rne(a - __uint_as_float(hi << 16));
-}
-
 // Tile t of a launch -> (segment, expert, m tile, n tile); both CTAs of a pair decode the same
 // tile.  M tiles fastest: the CTAs sharing one weight tile run side by side, so the weights
 // cross HBM once and the (L2-resident) token tiles are the ones re-read.
@@ -179,7 +173,6 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
           } else {
             while (kin >= p.seg[s].nrows / kPfBK) { ++s; kin = 0; }
             tma2d<CG>(sa, &p.tmA, p.seg[s].row0 + kin * kPfBK, arow, fb);
-            tma2d<CG>(sa + kABytes, &p.tmA2, p.seg[s].row0 + kin * kPfBK, arow, fb);
             // B (MN-major down columns): this CTA's 256 / CG output columns
 #pragma unroll
             for (int j = 0; j < 4 / CG; ++j)
@@ -194,7 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
     if (lane == 0 && rank == 0) {
       // gate/up: B_gate and B_up are adjacent 128-row K-major blocks, i.e. one 256-row operand
       // (CG = 1) or one 128-row half per CTA (CG = 2), so one N = 256 MMA computes [D_g | D_u]
-      constexpr uint32_t idesc = DOWN ? make_idesc(kTM, kPfBN2, 1) : make_idesc(kTM, 2 * kPfBN1, 0);
+      // down: fp16 a x fp16 down columns (reading Q31); gate/up: bf16 x bf16
+      constexpr uint32_t idesc = DOWN ? make_idesc(kTM, kPfBN2, 1, 0, 1) : make_idesc(kTM, 2 * kPfBN1, 0);
       int it = 0, j = 0;
       for (int t = c0; t < p.ntiles; t += G, ++j) {
         int seg, ex, mt, nt;
@@ -217,9 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
             if (!DOWN) {
               umma<CG>(d, da, desc_k_sw128(sb + k * 32), idesc, acc);
             } else {
-              const uint64_t db = desc_mn_sw128(sb + k * 2048, 8192, 1024);
-              umma<CG>(d, da, db, idesc, acc);
-              umma<CG>(d, desc_k_sw128(sa + kABytes + k * 32), db, idesc, 1u);   // + A_lo * B
+              umma<CG>(d, da, desc_mn_sw128(sb + k * 2048, 8192, 1024), idesc, acc);
             }
           }
           umma_commit<CG>(&empty[st]);
@@ -250,29 +242,21 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
         const PfSeg S = p.seg[seg];
         const size_t off = (size_t)(arow + m) * p.ld_out + S.row0 + nt * kPfBN1;
         uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + off;
-        uint16_t* out_lo = reinterpret_cast<uint16_t*>(p.out2) + off;
         for (int c = half * (kPfBN1 / 2); c < (half + 1) * (kPfBN1 / 2); c += 16) {
           float g[16], u[16];
           tmem_ld16(tbase + c, g);
           tmem_ld16(tbase + kPfBN1 + c, u);
           if (row_ok && nt * kPfBN1 + c < S.nrows) {
-            uint32_t ph[8], pl[8];
+            uint32_t ph[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
               const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
-              uint32_t h0, l0, h1, l1;
-              split_bf16(a0, h0, l0);
-              split_bf16(a1, h1, l1);
-              ph[i] = h0 | (h1 << 16);
-              pl[i] = l0 | (l1 << 16);
+              ph[i] = f16_sat(a0) | (f16_sat(a1) << 16);   // fp16 a (reading Q31)
             }
             uint4* o = reinterpret_cast<uint4*>(out + c);
             o[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
             o[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
-            uint4* ol = reinterpret_cast<uint4*>(out_lo + c);
-            ol[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-            ol[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
           }
         }
       } else {

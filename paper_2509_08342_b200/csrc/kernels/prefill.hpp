@@ -33,8 +33,7 @@ struct PfExpert {
 };
 
 struct PfGemmParams {
-  CUtensorMap tmA;                    // A operand: X_perm (gate/up) or A_act hi (down), 2-D
-  CUtensorMap tmA2;                   // down: A_act lo (a = hi + lo)
+  CUtensorMap tmA;                    // A operand: X_perm (gate/up, bf16) or A_act (down, fp16), 2-D
   CUtensorMap tmB[kPfMaxSegs];        // weight segments, 3-D {d, 3, rows}
   PfSeg seg[kPfMaxSegs];
   PfExpert ex[kPfMaxExperts];
@@ -42,8 +41,7 @@ struct PfGemmParams {
   int32_t ntiles;                     // total output tiles of the launch (CTA pairs if cta_pair)
   int32_t cta_pair;                   // 1: cta_group::2 pairs, 256-row tiles (UMMA M = 256)
   int32_t d, I;
-  void* out;                          // gate/up: bf16 A_act hi [rows][I]; down: fp32 Y [rows][d]
-  void* out2;                         // gate/up: bf16 A_act lo [rows][I]
+  void* out;                          // gate/up: fp16 A_act [rows][I]; down: fp32 Y [rows][d]
   int32_t ld_out;                     // elements per output row
   int32_t accumulate;                 // down: add into `out` (second segment group)
 };

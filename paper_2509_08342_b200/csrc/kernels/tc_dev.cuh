@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "device_utils.cuh"
 
@@ -20,11 +21,16 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo, 
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn, int a_mn = 0) {
-  // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1), A K-major,
-  // A major bit 15, B major bit 16, N >> 3 at bit 17, M >> 4 at bit 24
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn, int a_mn = 0, int f16 = 0) {
+  // kind::f16: D fp32 (bit 4), A / B bf16 (bits 7-9 / 10-12 = 1) or fp16 (0), A major bit 15,
+  // B major bit 16 (1 = MN-major), N >> 3 at bit 17, M >> 4 at bit 24
+  return (1u << 4) | ((uint32_t)(f16 ? 0 : 1) << 7) | ((uint32_t)(f16 ? 0 : 1) << 10) | ((uint32_t)a_mn << 15) |
+         ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// fp32 -> fp16 bits, round to nearest even, saturated to +-65504 (activations of the down MMAs)
+__device__ __forceinline__ uint32_t f16_sat(float a) {
+  const float c = fminf(fmaxf(a, -65504.f), 65504.f);
+  return (uint32_t)__half_as_ushort(__float2half_rn(c));
 }
 
 template <int CG>

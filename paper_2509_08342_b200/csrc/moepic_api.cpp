@@ -152,7 +152,7 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
     const uint64_t T = d.max_batch;
     a.pf_rows = T * d.K + (uint64_t)d.N * (kPfBM - 1) + (uint64_t)d.n_shared * (T + kPfBM - 1) + kPfBM;
     a.xperm = off; off = align_up(off + a.pf_rows * d.d * 2, 1024);
-    a.aact = off; off = align_up(off + a.pf_rows * d.I * 4, 1024);
+    a.aact = off; off = align_up(off + a.pf_rows * d.I * 2, 1024);
     a.yperm = off; off = align_up(off + a.pf_rows * d.d * 4);
     a.pos = off; off = align_up(off + T * d.K * 4);
     a.cursor = off; off = align_up(off + (size_t)d.N * 4);
@@ -639,6 +639,28 @@ moepic_status moepic_load_router(moepic_ctx* ctx, int32_t layer, const uint16_t*
 
 // HF layout -> row-interleaved rows [gate_r | up_r | down[:, r]] for r in [r0, r0 + I); the HF
 // tensors hold I_full rows (gate/up [I_full][d], down [d][I_full]); r0 = tp_rank * I.
+// The down column of a stored bf16 row is re-encoded as fp16 (reading Q31): exact for
+// every bf16 value of magnitude in [2^-14, 65280] (the bf16 mantissa has 8 bits, fp16's 11), round
+// to nearest even below 2^-14 (fp16 subnormals, absolute error <= 2^-25).  The down-projection
+// MMAs then take an fp16 activation: one MMA per K step with an 11-bit activation mantissa.
+static inline uint16_t bf16_to_f16(uint16_t b) {
+  const uint32_t sign = (uint32_t)(b & 0x8000u);
+  const uint32_t ax = (uint32_t)(b & 0x7FFFu) << 16;   // |x| as fp32 bits
+  if (ax >= 0x47800000u) return (uint16_t)(sign | 0x7C00u | (ax > 0x7F800000u ? 0x200u : 0u));   // >= 2^16: inf / nan
+  if (ax < 0x38800000u) {   // below 2^-14: fp16 subnormal (or zero), value = round(|x| * 2^24)
+    float v;
+    memcpy(&v, &ax, 4);
+    return (uint16_t)(sign | (uint32_t)std::nearbyint(v * 16777216.0f));
+  }
+  return (uint16_t)(sign | ((((ax >> 23) - 112u) << 10) | ((ax >> 13) & 0x3FFu)));   // exact: 7-bit mantissa
+}
+// load_expert rejects down weights fp16 cannot hold (|x| >= 65536 or not finite)
+static inline bool down_fits_f16(const uint16_t* down, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if ((down[i] & 0x7FFFu) >= 0x4780u) return false;
+  return true;
+}
+
 static void pack_rows_bf16(uint8_t* dst, const uint16_t* gate, const uint16_t* up, const uint16_t* down, int d,
                            int I, int r0, int I_full) {
   gate += (size_t)r0 * d;
@@ -657,7 +679,7 @@ static void pack_rows_bf16(uint8_t* dst, const uint16_t* gate, const uint16_t* u
       const int ke = std::min(d, k0 + 64);
       for (int r = rb; r < re; ++r) {
         uint16_t* orow = o + (size_t)r * rowe + 2 * d;
-        for (int k = k0; k < ke; ++k) orow[k] = down[(size_t)k * I_full + r];
+        for (int k = k0; k < ke; ++k) orow[k] = bf16_to_f16(down[(size_t)k * I_full + r]);
       }
     }
   }
@@ -743,6 +765,8 @@ moepic_status moepic_load_expert(moepic_ctx* ctx, int32_t layer, int32_t expert,
   CTX_GUARD();
   const auto& d = ctx->desc;
   if (!gate || !up || !down) return fail(&ctx->err, MOEPIC_EINVAL, "weight pointer is NULL");
+  if (d.weight_format == MOEPIC_BF16 && !down_fits_f16(down, (size_t)d.d * ctx->I_full))
+    return fail(&ctx->err, MOEPIC_EINVAL, "down weight outside the fp16 range of the stored row (|x| >= 65536)");
   if (expert >= 0) {
     if (expert >= d.N) return fail(&ctx->err, MOEPIC_EINVAL, "expert out of range");
     if (layer < 0 || layer >= d.L_host) return fail(&ctx->err, MOEPIC_EINVAL, "layer must be < L_host");
@@ -769,6 +793,7 @@ moepic_status moepic_pack_expert(const moepic_model_desc* desc, const uint16_t* 
     return MOEPIC_OK;
   }
   if (*bytes < need || !gate || !up || !down) return MOEPIC_EINVAL;
+  if (l.weight_format == MOEPIC_BF16 && !down_fits_f16(down, (size_t)l.d * desc->I)) return MOEPIC_EINVAL;
   pack_rows(l, static_cast<uint8_t*>(out), gate, up, down, desc->I);
   *bytes = need;
   return MOEPIC_OK;
@@ -1258,8 +1283,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   }
   if ((uint64_t)rows + kPfBM > ctx->lay.pf_rows) return fail(&ctx->err, MOEPIC_ERUNTIME, "prefill row overflow");
   uint16_t* xperm = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.xperm);
-  uint16_t* aact = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.aact);
-  uint16_t* aact_lo = aact + ctx->lay.pf_rows * d.I;   // a = hi + lo
+  uint16_t* aact = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.aact);   // fp16 a (reading Q31)
   float* Y = reinterpret_cast<float*>(ctx->arena + ctx->lay.yperm);
   int32_t* pos = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.pos);
   int32_t* cursor = reinterpret_cast<int32_t*>(ctx->arena + ctx->lay.cursor);
@@ -1278,10 +1302,9 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   ++launches;
 
   PfGemmParams& gp = *ctx->pf_gp;
-  CUtensorMap tm_x, tm_act, tm_act_lo;
+  CUtensorMap tm_x, tm_act;
   if (!pf_tmap_2d(&tm_x, xperm, (uint64_t)rows + kPfBM, d.d, kPfBM) ||
-      !pf_tmap_2d(&tm_act, aact, (uint64_t)rows + kPfBM, d.I, kPfBM) ||
-      !pf_tmap_2d(&tm_act_lo, aact_lo, (uint64_t)rows + kPfBM, d.I, kPfBM))
+      !pf_tmap_2d(&tm_act, aact, (uint64_t)rows + kPfBM, d.I, kPfBM))
     return fail(&ctx->err, MOEPIC_ERUNTIME, "cuTensorMapEncodeTiled failed (activations)");
   auto tidx = [&](int expert) { return expert >= 0 ? expert : N + (-1 - expert); };
   // gate/up runs on CTA pairs (UMMA M = 256: half the B operand bytes per SM; ncu: tensor pipe
@@ -1321,7 +1344,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
       }
       gp.ntiles = (int32_t)tiles;
       gp.cta_pair = CGu == 2;
-      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.out2 = aact_lo; gp.ld_out = d.I; gp.accumulate = 0;
+      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.ld_out = d.I; gp.accumulate = 0;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
       launch_pf_gateup(gp, s);
       ctx->prof_end(pe, s, (uint64_t)flops);
@@ -1339,7 +1362,6 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
         i1 = j;
       }
       gp.tmA = tm_act;
-      gp.tmA2 = tm_act_lo;
       gp.nseg = (int)(i1 - i0);
       gp.nexp = NE;
       for (int e = 0; e < NE; ++e) {

@@ -113,7 +113,34 @@ def test_library_packer_matches_oracle_bit_for_bit(d, I, tp):
         desc = api.model_desc(1, 4, 2, d, I, row_granule=16, tp_rank=r, tp_size=tp, weight_format=api.M.Q4G64)
         img = api.pack_expert(desc, gate, up, down).reshape(I // tp, -1)
         assert np.array_equal(img, ref[r * I // tp:(r + 1) * I // tp])
-    # bf16 format: the plain interleaved rows [gate_r | up_r | down[:, r]]
+    # bf16 format: the interleaved rows [gate_r | up_r | down[:, r]], the down column as fp16
+    # (reading Q31): numpy's IEEE round-to-nearest-even float16 conversion of the bf16 values
     desc = api.model_desc(1, 4, 2, d, I, row_granule=16)
     img = api.pack_expert(desc, gate, up, down).view(np.uint16).reshape(I, 3, d)
-    assert np.array_equal(img[:, 0], gate) and np.array_equal(img[:, 1], up) and np.array_equal(img[:, 2], down.T)
+    down_f16 = synth.bits_to_bf16(np.ascontiguousarray(down.T)).float().numpy().astype(np.float16).view(np.uint16)
+    assert np.array_equal(img[:, 0], gate) and np.array_equal(img[:, 1], up) and np.array_equal(img[:, 2], down_f16)
+
+
+def test_down_column_fp16_reencoding():
+    """Reading Q31: the stored down column is fp16.  Pins of the host packer's bf16 -> fp16
+    conversion: exact (round trip) over the whole bf16 range [2^-14, 65280] of both signs;
+    round-to-nearest-even subnormals below 2^-14 against numpy; +-0 kept; |x| >= 65536 rejected."""
+    from paper_2509_08342_b200 import api
+    allb = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    fin = allb[(allb & 0x7FFF) < 0x4780]                                # every bf16 fp16 can hold
+    d, I = 64, len(fin) // 64 // 16 * 16
+    fin = fin[:d * I]
+    down = np.ascontiguousarray(fin.reshape(I, d).T)                    # [d][I]: column r = row r
+    z = np.zeros((I, d), np.uint16)
+    desc = api.model_desc(1, 4, 2, d, I, row_granule=16)
+    img = api.pack_expert(desc, z, z, down).view(np.uint16).reshape(I, 3, d)[:, 2].ravel()
+    x = synth.bits_to_bf16(fin).float().numpy()
+    ref = x.astype(np.float16)
+    assert np.array_equal(img, ref.view(np.uint16))
+    normal = np.abs(x) >= 2.0 ** -14
+    assert np.array_equal(ref[normal].astype(np.float32), x[normal])     # exact where fp16 is normal
+    assert np.abs(ref.astype(np.float64) - x)[~normal].max() <= 2.0 ** -25
+    bad = down.copy()
+    bad[0, 0] = 0x4780                                                   # 65536: does not fit
+    with pytest.raises(Exception):
+        api.pack_expert(desc, z, z, bad)
