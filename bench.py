@@ -238,9 +238,12 @@ def run_ours(args, log):
     y_cap = S.K * B if args.y_cap is None else args.y_cap
     base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[y_cap] * L, seed=0)
     window_rows = None
-    if args.prefetch_window_us > 0:   # reading Q30: the link-idle window per layer, in expert rows
-        rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
-        window_rows = int(args.prefetch_window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
+    window_us = None
+    rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
+    auto_window = args.prefetch_window_us == "auto" and cfg.get("adaptive") and not cfg.get("prefill")
+    if args.prefetch_window_us not in ("auto", "0", "0.0"):   # reading Q30: a fixed window per layer
+        window_us = float(args.prefetch_window_us)
+        window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
         base_cfg["prefetch_rows_i"] = [window_rows] * L
     mode = MODES[args.mode]
     if "theta" in mode:
@@ -260,6 +263,8 @@ def run_ours(args, log):
         ctx.join_process_group(api.M.TRANSPORT_NCCL if transport == "nccl" else api.M.TRANSPORT_PEER)
         log(f"[bench] rank {rank} joined the {parallel} group ({transport} transport)")
     adapt_tokens = 2 * args.tau if cfg.get("adaptive") else 0
+    cal_tokens = 8 if auto_window else 0   # link-idle calibration after Alg. 1 (reading Q30)
+    adapt_tokens += cal_tokens
     T = adapt_tokens + args.warmup + args.steps
     # token t, layer i uses rows [t*B, (t+1)*B) of a [T*B][L][d] organic hidden-state process
     # stored [L][tokens][d] so every per-layer batch slice is a contiguous [B][d] block
@@ -329,25 +334,49 @@ def run_ours(args, log):
         # Alg. 1 outer loop: run 2 tau tokens on the uniform theta = 0.5 layout, profile
         # T_moe on this GPU and T_load^exp = U_e / PCIe, then reconfigure with the solver.
         ctx.profile(True)
-        for t in range(adapt_tokens):
+        for t in range(adapt_tokens - cal_tokens):
             step(t)
         torch.cuda.synchronize()
         k2w = ctx.profile_read(api.M.KERNEL_EXPERT)
         ctx.profile(False)
         rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
         U_e = rbytes * (S.I // world if parallel == "tp" else S.I)   # bytes of one (local) expert
-        t_moe_measured = k2w["total_ms"] / (adapt_tokens * L)      # ms of expert compute per layer-step
+        t_moe_measured = k2w["total_ms"] / ((adapt_tokens - cal_tokens) * L)   # ms of expert compute per layer-step
         if args.alg1_inputs == "measured":
             t_load = U_e / (pcie * 1e9) * 1e3                      # ms per full expert
             t_moe = t_moe_measured
         else:   # fixed, modelled profile (reproducible run to run): link and HBM rates
             t_load = U_e / (ALG1_PCIE_GBS * 1e9) * 1e3             # of this pool's boxes, K experts'
             t_moe = S.K * B * U_e / (ALG1_HBM_GBS * 1e9) * 1e3 + ALG1_LAUNCH_MS   # rows + launch cost
+        if cal_tokens:
+            # the prefetch window of this stack (P:389 / P:412 T_wind, reading Q30): with no
+            # attention block the link idles per layer for the serial chain final K2 -> router ->
+            # host -> first copy.  Measured as (layer time - PCIe bytes / link rate) over the last
+            # cal_tokens adaptation tokens (no timing events), rounded to 10 us so the configuration
+            # reproduces run to run; the plan of every layer is cut at that many rows of link time.
+            # It is not fed back into Alg. 1 as T_att: re-solving with it moved DeepSeek to smaller
+            # theta and lost 3.5 % (Mixtral 0.9 %) against the cut alone (Q30).
+            cc0 = ctx.counters()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for t in range(adapt_tokens - cal_tokens, adapt_tokens):
+                step(t)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            cc1 = ctx.counters()
+            lay_ms = a0.elapsed_time(a1) / (cal_tokens * L)
+            link_ms = (cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] - cc0["pcie_ondemand_bytes"]
+                       - cc0["pcie_prefetch_bytes"]) / (cal_tokens * L) / (ALG1_PCIE_GBS * 1e9) * 1e3
+            window_us = max(0.0, round((lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
+            window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
+            base_cfg["prefetch_rows_i"] = [window_rows] * L
+            log(f"[bench] link-idle window {window_us:.0f} us per layer ({window_rows} rows)")
         t0 = time.time()
         solved = ctx.configure(use_solver=True, t_att=t_att, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
                                zeta=0.01, **{k: v for k, v in base_cfg.items() if k != "theta_i"})
+        t_att_alg1 = t_att
         alg1_in = {"inputs": args.alg1_inputs, "t_load_exp_ms": round(t_load, 6), "t_moe_ms": round(t_moe, 6),
-                   "t_att_ms": round(t_att, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
+                   "t_att_ms": round(t_att_alg1, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
         log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(solved['theta_eff_i']):.2f}.."
             f"{max(solved['theta_eff_i']):.2f}, C {min(solved['C_i'])}..{max(solved['C_i'])}")
     for t in range(adapt_tokens, adapt_tokens + args.warmup):
@@ -356,7 +385,11 @@ def run_ours(args, log):
     if dist:
         dist.barrier()
     c0 = ctx.counters()
-    ctx.profile(not args.no_kernel_events)
+    # time the dominant kernel only (the roofline's); every timing-event pair sits on the compute
+    # stream's critical path (--kernel-events all also times the router and the combine)
+    prof_classes = (api.M.PROFILE_CLASSES | (1 << api.M.KERNEL_EXPERT) | (1 << api.M.KERNEL_GEMM)
+                    if args.kernel_events == "dominant" else 1)
+    ctx.profile(0 if args.no_kernel_events else prof_classes)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
@@ -497,7 +530,8 @@ def run_ours(args, log):
                                                              theta_eff_i=[round(x, 4) for x in solved["theta_eff_i"]],
                                                              C_i=solved["C_i"]),
                    "y_cap": y_cap, "prefetch_window": None if window_rows is None else
-                   {"us": args.prefetch_window_us, "rows": window_rows},
+                   {"us": window_us, "rows": window_rows, "source": "measured link idle (auto)" if auto_window
+                    else "--prefetch-window-us"},
                    "build_id": _build.build_id(),
                    "l2": "inputs larger than L2 (>=700 MB of expert rows streamed per layer)"},
         "layer_latency_us": {"mean": round(layer_us, 2),
@@ -698,10 +732,13 @@ def main():
                          "nccl = a library-owned NCCL communicator")
     ap.add_argument("--alg1-inputs", default="model", choices=["model", "measured"],
                     help="Alg. 1 profile: fixed model of the box (reproducible, default) or this run's timings")
+    ap.add_argument("--kernel-events", default="dominant", choices=["dominant", "all"],
+                    help="timing events around the dominant kernel's launches only (default) or every kernel")
     ap.add_argument("--y-cap", type=int, default=None, help="prefetch count cap per layer (default K*B)")
-    ap.add_argument("--prefetch-window-us", type=float, default=0.0,
-                    help="reading Q30: cut each layer's prefetch plan at this many microseconds of link time "
-                         "(0 = no window: Alg. 1's Y caps the plan)")
+    ap.add_argument("--prefetch-window-us", default="auto",
+                    help="reading Q30: cut each layer's prefetch plan at this many microseconds of link time; "
+                         "auto (adaptive decode configs) = the measured per-layer link-idle time, also Alg. 1's "
+                         "T_att; 0 = no window (Alg. 1's Y caps the plan)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.e2e_steps is None:

@@ -256,7 +256,11 @@ typedef struct {
 } moepic_kernel_stats;
 enum { MOEPIC_KERNEL_ROUTER = 0, MOEPIC_KERNEL_EXPERT = 1, MOEPIC_KERNEL_COMBINE = 2,
        MOEPIC_KERNEL_GEMM = 3 /* prefill tcgen05 GEMMs; `bytes` holds algorithmic FLOPs */ };
-/* enable != 0 starts (and resets) event timing; 0 stops it.                                   */
+/* enable != 0 starts (and resets) event timing; 0 stops it.  enable = 1 times every class;
+ * enable = MOEPIC_PROFILE_CLASSES | (1 << class) | ... times only those classes (each timing event
+ * pair sits on the compute stream's critical path: ~4 us per record, more under a saturated H2D
+ * link).                                                                        */
+enum { MOEPIC_PROFILE_CLASSES = 0x100 };
 moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable);
 /* Synchronises the recorded events and returns the totals for one kernel class.               */
 moepic_status moepic_profile_read(moepic_ctx* ctx, int32_t kernel_class, moepic_kernel_stats* out);

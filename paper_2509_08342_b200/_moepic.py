@@ -75,6 +75,7 @@ class moepic_kernel_stats(C.Structure):
 
 
 KERNEL_ROUTER, KERNEL_EXPERT, KERNEL_COMBINE, KERNEL_GEMM = 0, 1, 2, 3
+PROFILE_CLASSES = 0x100   # moepic_profile: time only the classes whose bits are set
 
 _ctxp = C.c_void_p
 _sig = {

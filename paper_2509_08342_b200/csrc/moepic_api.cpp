@@ -451,8 +451,9 @@ struct moepic_ctx {
   size_t prof_used = 0;
   moepic_kernel_stats prof_acc[4]{};
 
+  uint32_t prof_mask = 0xF;   // kernel classes timed (moepic_profile)
   int prof_begin(cudaStream_t s, int cls) {
-    if (!profiling) return -1;
+    if (!profiling || !((prof_mask >> cls) & 1u)) return -1;
     if (prof_used == prof.size()) {
       ProfEv e{};
       if (cudaEventCreate(&e.a) != cudaSuccess || cudaEventCreate(&e.b) != cudaSuccess) return -1;
@@ -2248,6 +2249,7 @@ moepic_status moepic_profile(moepic_ctx* ctx, int32_t enable) {
   ctx->prof_drain();
   for (auto& k : ctx->prof_acc) k = moepic_kernel_stats{};
   ctx->profiling = enable != 0;
+  ctx->prof_mask = (enable & MOEPIC_PROFILE_CLASSES) ? (uint32_t)(enable & 0xF) : 0xFu;
   if (ctx->profiling) {
     ctx->tstamp_reset(kProfRing);
     if (cudaDeviceSynchronize() != cudaSuccess) return fail(&ctx->err, MOEPIC_ERUNTIME, "profile reset failed");
