@@ -101,8 +101,9 @@ typedef struct {
                              of 64 to 4-bit codes with a bf16 scale and minimum (DESIGN.md
                              reading Q28); K2 dequantises on the fly (fp32 accumulation).  A
                              row then takes 27d/16 bytes (padded to 16) instead of 6d, so every
-                             PCIe and HBM byte count shrinks ~3.5x.  Needs d % 64 == 0 and
-                             max_batch <= 32 (decode; the tcgen05 prefill GEMMs are bf16).     */
+                             PCIe and HBM byte count shrinks ~3.5x.  Needs d % 64 == 0.  Prefill
+                             batches (> 32 tokens) dequantise each segment group once into fp16
+                             rows for the tcgen05 GEMMs (reading Q32).                         */
 } moepic_model_desc;
 enum { MOEPIC_BF16 = 0, MOEPIC_Q4G64 = 1 };
 

@@ -187,8 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1) pf_gemm(const __grid_constant__ P
     if (lane == 0 && rank == 0) {
       // gate/up: B_gate and B_up are adjacent 128-row K-major blocks, i.e. one 256-row operand
       // (CG = 1) or one 128-row half per CTA (CG = 2), so one N = 256 MMA computes [D_g | D_u]
-      // down: fp16 a x fp16 down columns (reading Q31); gate/up: bf16 x bf16
-      constexpr uint32_t idesc = DOWN ? make_idesc(kTM, kPfBN2, 1, 0, 1) : make_idesc(kTM, 2 * kPfBN1, 0);
+      // down: fp16 a x fp16 down columns (reading Q31); gate/up: bf16 x bf16, or fp16 x fp16 for
+      // dequantised Q4G64 rows (reading Q32)
+      const uint32_t idesc = DOWN ? make_idesc(kTM, kPfBN2, 1, 0, 1)
+                                  : (p.f16 ? make_idesc(kTM, 2 * kPfBN1, 0, 0, 1) : make_idesc(kTM, 2 * kPfBN1, 0));
       int it = 0, j = 0;
       for (int t = c0; t < p.ntiles; t += G, ++j) {
         int seg, ex, mt, nt;
@@ -323,7 +325,48 @@ __global__ void pf_permute(const __grid_constant__ PfPermuteParams p) {
   }
   const uint4* src = reinterpret_cast<const uint4*>(p.h + (size_t)t * p.d);
   uint4* dst = reinterpret_cast<uint4*>(p.xperm + (size_t)row * p.d);
-  for (int c = lane; c < p.d / 8; c += 32) dst[c] = src[c];
+  if (!p.f16) {
+    for (int c = lane; c < p.d / 8; c += 32) dst[c] = src[c];
+  } else {   // bf16 -> fp16: exact for |h| in [2^-14, 65504] (saturated beyond)
+    for (int c = lane; c < p.d / 8; c += 32) {
+      const uint4 v = src[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = f16_sat(bf16lo(w[i])) | (f16_sat(bf16hi(w[i])) << 16);
+      dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+// Q4G64 rows -> fp16 rows (reading Q32): one warp per row; lane j takes code words j, j + 32, ...
+// (8 codes of one 64-column group each: x' = lo_b + code * s_b in fp32, rounded once to fp16)
+__global__ void pf_dequant(const __grid_constant__ PfDequantParams p) {
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gw >= p.total_rows) return;
+  int s = 0;
+  while (s + 1 < p.nseg && p.seg[s + 1].row_begin <= gw) ++s;
+  const int r = gw - p.seg[s].row_begin;
+  const uint8_t* row = p.seg[s].src + (size_t)r * p.src_row_bytes;
+  uint4* out = reinterpret_cast<uint4*>(p.seg[s].dst + (size_t)r * 3 * p.d);
+  const int d = p.d, words = 3 * d / 8, wpp = d / 8;   // code words per row / per part
+  const uint32_t* codes = reinterpret_cast<const uint32_t*>(row);
+  const uint32_t* prm = reinterpret_cast<const uint32_t*>(row + 3 * (d / 2));
+  for (int w = lane; w < words; w += 32) {
+    const int part = w / wpp, col = (w - part * wpp) * 8;
+    const uint32_t pr = __ldg(prm + part * (d >> 6) + (col >> 6));
+    const float sc = __uint_as_float(pr << 16), mn = __uint_as_float(pr & 0xFFFF0000u);
+    const uint32_t c = __ldg(codes + w);
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float q0 = __uint_as_float(0x4B000000u | ((c >> (8 * i)) & 15u)) - 8388608.0f;
+      const float q1 = __uint_as_float(0x4B000000u | ((c >> (8 * i + 4)) & 15u)) - 8388608.0f;
+      o[i] = f16_sat(fmaf(q0, sc, mn)) | (f16_sat(fmaf(q1, sc, mn)) << 16);
+    }
+    out[w] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
 }
 
 __global__ void pf_combine(const __grid_constant__ PfCombineParams p) {
@@ -426,6 +469,10 @@ void launch_pf_down(const PfGemmParams& p, cudaStream_t s) {
 void launch_pf_permute(const PfPermuteParams& p, cudaStream_t s) {
   const int warps = p.T * p.K + p.n_shared * p.T;
   pf_permute<<<(warps + 7) / 8, 256, 0, s>>>(p);
+}
+void launch_pf_dequant(const PfDequantParams& p, cudaStream_t s) {
+  if (p.total_rows <= 0) return;
+  pf_dequant<<<(p.total_rows + 7) / 8, 256, 0, s>>>(p);
 }
 void launch_pf_combine(const PfCombineParams& p, cudaStream_t s) {
   dim3 grid((unsigned)((p.d / 4 + 127) / 128), (unsigned)p.T);

@@ -44,7 +44,22 @@ struct PfGemmParams {
   void* out;                          // gate/up: fp16 A_act [rows][I]; down: fp32 Y [rows][d]
   int32_t ld_out;                     // elements per output row
   int32_t accumulate;                 // down: add into `out` (second segment group)
+  int32_t f16;                        // gate/up operands fp16 (Q4G64 experts, reading Q32)
 };
+
+// Q4G64 prefill (reading Q32): the step's segments are dequantised once into fp16 rows
+// [gate | up | down] (6d bytes, the bf16 row geometry) so the GEMMs read them like bf16 rows.
+struct PfDequantSeg {
+  const uint8_t* src;       // packed Q4G64 rows
+  uint16_t* dst;            // fp16 rows
+  int32_t nrows;
+  int32_t row_begin;        // prefix over the launch's segments
+};
+struct PfDequantParams {
+  int32_t nseg, d, src_row_bytes, total_rows;
+  PfDequantSeg seg[kPfMaxSegs];
+};
+void launch_pf_dequant(const PfDequantParams& p, cudaStream_t s);
 
 // Tensor maps (driver entry point resolved at runtime; no -lcuda).
 bool pf_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
@@ -64,6 +79,7 @@ struct PfPermuteParams {
   int T, K, d;
   int e_lo, e_hi;           // local experts [e_lo, e_hi)
   int n_shared;             // shared expert s: all T tokens at rows shared_off[s] + t
+  int f16;                  // write X as fp16 (Q4G64 prefill, reading Q32)
   int32_t shared_off[8];
   int32_t m_off[kPfMaxExperts];   // first padded row of each routed expert's block
 };

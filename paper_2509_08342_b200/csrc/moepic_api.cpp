@@ -45,8 +45,8 @@ struct ArenaLayout {
   size_t routers, shared, pool, buf[2], ws, logits, ids, w, ranking, ticket, rsel, trec, hstage, ystage, total;
   uint64_t pool_rows, plan_rows, od_rows, ws_floats, map_rows;
   // prefill (max_batch > kDecodeMaxB): permuted tokens, intermediate activations, outputs
-  size_t xperm, aact, yperm, pos, cursor;
-  uint64_t pf_rows;
+  size_t xperm, aact, yperm, pos, cursor, wdq;
+  uint64_t pf_rows, wdq_rows;
 };
 constexpr int kDecodeMaxB = 32;   // decode path (K2) serves up to 32 tokens (token bit masks)
 
@@ -82,8 +82,7 @@ std::string validate_desc(const moepic_model_desc* d) {
   if (d->tp_size > 1 && d->ep_size != 1) return "tp_size > 1 needs ep_size == 1";
   if (d->I % ((int64_t)d->tp_size * d->row_granule) != 0) return "I must be a multiple of tp_size * row_granule";
   if (d->weight_format != MOEPIC_BF16 && d->weight_format != MOEPIC_Q4G64) return "weight_format invalid";
-  if (d->weight_format == MOEPIC_Q4G64 && (d->d % 64 != 0 || d->max_batch > kDecodeMaxB))
-    return "Q4G64 experts need d % 64 == 0 and max_batch <= 32";
+  if (d->weight_format == MOEPIC_Q4G64 && d->d % 64 != 0) return "Q4G64 experts need d % 64 == 0";
   if (d->max_batch > kDecodeMaxB && (d->row_granule % 64 != 0 || (d->I / d->tp_size) % 64 != 0))
     return "prefill batches (max_batch > 32) need row_granule and I / tp_size to be multiples of 64 (GEMM K tiles)";
   return "";
@@ -146,8 +145,8 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
   a.hstage = off; off = align_up(off + (size_t)d.max_batch * d.d * 2);   // layer_forward_host input rows
   a.ystage = off;                                                          // ... and prefill outputs
   if (d.max_batch > kDecodeMaxB) off = align_up(off + (size_t)d.max_batch * d.d * 4);
-  a.pf_rows = 0;
-  a.xperm = a.aact = a.yperm = a.pos = a.cursor = off;
+  a.pf_rows = a.wdq_rows = 0;
+  a.xperm = a.aact = a.yperm = a.pos = a.cursor = a.wdq = off;
   if (d.max_batch > kDecodeMaxB) {
     const uint64_t T = d.max_batch;
     a.pf_rows = T * d.K + (uint64_t)d.N * (kPfBM - 1) + (uint64_t)d.n_shared * (T + kPfBM - 1) + kPfBM;
@@ -156,6 +155,10 @@ ArenaLayout arena_layout(const moepic_model_desc& d) {
     a.yperm = off; off = align_up(off + a.pf_rows * d.d * 4);
     a.pos = off; off = align_up(off + T * d.K * 4);
     a.cursor = off; off = align_up(off + (size_t)d.N * 4);
+    if (d.weight_format == MOEPIC_Q4G64) {   // reading Q32: one group's segments dequantised to fp16 rows
+      a.wdq_rows = (uint64_t)(Nl + d.n_shared) * d.I;
+      a.wdq = off; off = align_up(off + a.wdq_rows * 6ull * d.d, 1024);
+    }
   }
   a.total = off;
   return a;
@@ -343,6 +346,7 @@ struct moepic_ctx {
   std::unique_ptr<K2TParams> ktp = std::make_unique<K2TParams>();
   std::unique_ptr<PfPermuteParams> pf_pp = std::make_unique<PfPermuteParams>();
   std::unique_ptr<PfGemmParams> pf_gp = std::make_unique<PfGemmParams>();
+  std::unique_ptr<PfDequantParams> pf_dq = std::make_unique<PfDequantParams>();
   std::unique_ptr<CombineParams> cpar = std::make_unique<CombineParams>();
   std::unique_ptr<Group> grp;        // set by moepic_group_handle / moepic_group_join
   moepic_model_desc desc{};         // local shape: desc.I = I_full / tp_size rows per expert
@@ -1268,6 +1272,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   const auto& d = ctx->desc;
   const int N = d.N, K = d.K, NS = d.n_shared, NE = N + NS;
   const int lo_e = d.ep_rank * ctx->Nl(), hi_e = lo_e + ctx->Nl();
+  const bool q4 = d.weight_format == MOEPIC_Q4G64;
   std::vector<int32_t> cnt(NE, 0), moff(NE, 0);
   for (int i = 0; i < T * K; ++i) {
     const int e = ctx->ids_h[i];
@@ -1296,6 +1301,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   pp.h = h; pp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids); pp.cursor = cursor;
   pp.pos = pos; pp.xperm = xperm; pp.T = T; pp.K = K; pp.d = d.d; pp.e_lo = lo_e; pp.e_hi = hi_e;
   pp.n_shared = NS;
+  pp.f16 = q4 ? 1 : 0;
   for (int s2 = 0; s2 < NS; ++s2) pp.shared_off[s2] = moff[N + s2];
   for (int e = 0; e < N; ++e) pp.m_off[e] = moff[e];
   launch_pf_permute(pp, s);
@@ -1321,10 +1327,41 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   const int CGd = ctx->pf_cta_pair >= 0 ? (ctx->pf_cta_pair ? 2 : 1) : 1;
   auto ptiles = [&](int e, int CG) { return (int64_t)((table[e].mtiles + CG - 1) / CG); };
 
-  auto run_group = [&](const std::vector<StepSeg>& g) -> moepic_status {
-    for (const auto& sg : g)
+  auto run_group = [&](const std::vector<StepSeg>& g0) -> moepic_status {
+    for (const auto& sg : g0)
       if (sg.nrows % kPfBK != 0 || (reinterpret_cast<uintptr_t>(sg.base) & 15))
         return fail(&ctx->err, MOEPIC_ERUNTIME, "prefill segment rows must be a multiple of 64");
+    // Q4G64 (reading Q32): dequantise the group's segments once into fp16 rows; the GEMMs read those
+    std::vector<StepSeg> gq;
+    if (q4) {
+      gq = g0;
+      uint16_t* wdq = reinterpret_cast<uint16_t*>(ctx->arena + ctx->lay.wdq);
+      PfDequantParams& dq = *ctx->pf_dq;
+      int64_t next = 0;
+      for (size_t i0 = 0; i0 < gq.size(); i0 += kPfMaxSegs) {
+        const size_t i1 = std::min(gq.size(), i0 + (size_t)kPfMaxSegs);
+        dq.nseg = (int)(i1 - i0);
+        dq.d = d.d;
+        dq.src_row_bytes = (int)ctx->rb();
+        int rows_l = 0;
+        for (size_t i = i0; i < i1; ++i) {
+          if ((uint64_t)(next + gq[i].nrows) > ctx->lay.wdq_rows)
+            return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "dequant scratch overflow");
+          uint16_t* dst = wdq + (size_t)next * 3 * d.d;
+          dq.seg[i - i0] = PfDequantSeg{gq[i].base, dst, gq[i].nrows, rows_l};
+          gq[i].base = reinterpret_cast<const uint8_t*>(dst);
+          rows_l += gq[i].nrows;
+          next += gq[i].nrows;
+        }
+        dq.total_rows = rows_l;
+        const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
+        launch_pf_dequant(dq, s);
+        ctx->prof_end(pe, s, (uint64_t)rows_l * (ctx->rb() + 6ull * d.d));
+        CK(cudaGetLastError());
+        ++launches;
+      }
+    }
+    const std::vector<StepSeg>& g = q4 ? gq : g0;
     // gate/up: chunks of <= kPfMaxSegs segments
     for (size_t i0 = 0; i0 < g.size(); i0 += kPfMaxSegs) {
       const size_t i1 = std::min(g.size(), i0 + (size_t)kPfMaxSegs);
@@ -1345,7 +1382,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
       }
       gp.ntiles = (int32_t)tiles;
       gp.cta_pair = CGu == 2;
-      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.ld_out = d.I; gp.accumulate = 0;
+      gp.d = d.d; gp.I = d.I; gp.out = aact; gp.ld_out = d.I; gp.accumulate = 0; gp.f16 = q4 ? 1 : 0;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
       launch_pf_gateup(gp, s);
       ctx->prof_end(pe, s, (uint64_t)flops);
@@ -1388,7 +1425,7 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
       for (int e = 0; e < NE; ++e) tiles += (gp.ex[e].mtiles ? ptiles(e, CGd) : 0) * (d.d / kPfBN2);
       gp.ntiles = (int32_t)tiles;
       gp.cta_pair = CGd == 2;
-      gp.d = d.d; gp.I = d.I; gp.out = Y; gp.ld_out = d.d; gp.accumulate = 1;
+      gp.d = d.d; gp.I = d.I; gp.out = Y; gp.ld_out = d.d; gp.accumulate = 1; gp.f16 = 0;
       const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_GEMM);
       launch_pf_down(gp, s);
       ctx->prof_end(pe, s, (uint64_t)flops);
