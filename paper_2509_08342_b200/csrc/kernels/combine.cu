@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(kCombineWarps * 32) k3_combine(const __grid_co
   __shared__ float4 red[kCombineWarps * 32];
   extern __shared__ CombineSeg cs[];   // the segment table, walked per lane (see expert.cu)
   stamp_start(p.tstamp);
+  asm volatile("griddepcontrol.launch_dependents;");   // a PDL-launched router may get ready now
   for (int i = threadIdx.x; i < p.nsegs; i += blockDim.x) cs[i] = p.segs[i];
   __syncthreads();
   combine_block(blockIdx.x, cs, p.nsegs, p.ws, p.h, p.y, p.B, p.d, p.residual, red);
@@ -58,6 +59,20 @@ void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream
 __global__ void k0_trap() { __trap(); }
 
 void launch_trap(cudaStream_t s) { k0_trap<<<1, 1, 0, s>>>(); }
+
+__global__ void k0_stamp(unsigned long long* p) { *p = gtimer(); }
+void launch_stamp(unsigned long long* p, cudaStream_t s) { k0_stamp<<<1, 1, 0, s>>>(p); }
+// clock handshake (mapped host memory m): m[0] = 1 once running; waits for m[2] != 0 (written by
+// the host right after it read its own clock); m[1] = %globaltimer when it saw it
+__global__ void k0_clock_sync(volatile unsigned long long* m) {
+  m[0] = 1;
+  __threadfence_system();
+  while (m[2] == 0) {
+  }
+  m[1] = gtimer();
+  __threadfence_system();
+}
+void launch_clock_sync(unsigned long long* m, cudaStream_t s) { k0_clock_sync<<<1, 1, 0, s>>>(m); }
 
 cudaError_t combine_init() {
   cudaError_t e = cudaSuccess, r;

@@ -35,11 +35,22 @@ __device__ __forceinline__ unsigned long long* sig_of(uint8_t* base, const EpOff
   return reinterpret_cast<unsigned long long*>(base + of.sig) + phase * kEpMaxRanks + src;
 }
 
-// threads 0..G-1 of the CTA each wait for one source, then the CTA proceeds
+// threads 0..G-1 of the CTA each wait for one source, then the CTA proceeds.  A peer that never
+// signals (its process died) must not hang the GPU: after ~10 s of %globaltimer the wait traps,
+// the launch fails and the context is poisoned (ERUNTIME, then ESTATE).
 __device__ __forceinline__ void wait_all(const EpPeers& pr, const EpOffsets& of, int phase, unsigned long long epoch) {
   if (threadIdx.x < (unsigned)pr.G) {
     const unsigned long long* f = sig_of(pr.base[pr.me], of, phase, threadIdx.x);
-    while (ld_acquire_sys(f) < epoch) __nanosleep(64);
+    unsigned long long t0 = 0;
+    for (unsigned n = 0; ld_acquire_sys(f) < epoch; ++n) {
+      __nanosleep(64);
+      if ((n & 0xFFFF) == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (!t0) t0 = t;
+        else if (t - t0 > 10000000000ull) __trap();
+      }
+    }
   }
   __syncthreads();
   __threadfence_system();

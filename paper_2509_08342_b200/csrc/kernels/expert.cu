@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   const int64_t G = gridDim.x;
   const int64_t r0 = k2_row_lo(blockIdx.x, R, G), r1 = k2_row_lo(blockIdx.x + 1, R, G);
   stamp_start(p.tstamp);
+  asm volatile("griddepcontrol.launch_dependents;");   // a PDL-launched router may get ready now
   unsigned long long* dbg = p.dbg ? p.dbg + (size_t)blockIdx.x * 8 : nullptr;   // phase trace (tools)
   if (dbg && tid == 0) dbg[0] = gtimer();
   if (r0 >= r1) return;

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k2t_split_expert(const __grid_c
   const int nb = (u1 - u0 + 1) / 2;
   const int d = p.d;
   stamp_start(p.tstamp);
+  asm volatile("griddepcontrol.launch_dependents;");
   // MOEPIC_K2_TRACE: per CTA [start, MMA issue done, flush start, end (ns)] and wait cycles
   // [producer on empty, MMA on full, MMA issuing stages (+ waits on the epilogue << 40), epilogue on gu_full]
   unsigned long long* dbg = p.dbg ? p.dbg + (size_t)c * 8 : nullptr;

@@ -48,7 +48,9 @@ struct RouterParams {
 };
 constexpr int kRouterSplitB = 32;
 constexpr int kProfRing = 4096;   // profiling records (events + in-kernel timestamps) per drain
-void launch_router(const RouterParams& p, cudaStream_t s);
+// pdl: programmatic dependent launch after the previous kernel on s (its weight loads overlap
+// that kernel's tail; h is read after griddepcontrol.wait)
+void launch_router(const RouterParams& p, cudaStream_t s, bool pdl = false);
 cudaError_t router_init();     // shared-memory carveout hints (called by kernels_init)
 cudaError_t combine_init();
 
@@ -143,6 +145,9 @@ void launch_combine(const CombineParams& p, cudaStream_t s);
 void launch_stage_in(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
 // MOEPIC_FAULT_AT_STEP (tests): a one-thread kernel that executes a trap instruction
 void launch_trap(cudaStream_t s);
+// MOEPIC_TIMELINE (tools): one thread writes %globaltimer to *p when the stream reaches it
+void launch_stamp(unsigned long long* p, cudaStream_t s);
+void launch_clock_sync(unsigned long long* mapped, cudaStream_t s);
 
 // Attention stand-in (attention.cu): GQA decode over a KV cache [B][S_max][Hkv][dh], dh = 128.
 constexpr int kAttnChunk = 128;   // cache positions per split: one CTA (4 warps x 32) per split and kv head

@@ -19,6 +19,14 @@
 
 namespace moepic {
 
+// Mailbox words go to mapped pinned host memory with write-through stores: a plain store may sit
+// in L2 as a dirty system-memory line until later traffic evicts it (the host then saw the
+// routing hundreds of microseconds late, in proportion to the layer's HBM traffic; measured with
+// MOEPIC_TIMELINE), and a system-scope fence waits behind the saturated host->device link.
+__device__ __forceinline__ void st_wt(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.global.wt.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ bool key_better(double av, int aid, double bv, int bid) {
   return av > bv || (av == bv && aid < bid);
 }
@@ -159,6 +167,8 @@ __global__ void __launch_bounds__(256, CPL <= 8 ? 2 : 1) k1_router(RouterParams 
   // is issued before the first add (one memory latency), then the lane adds its exact products
   // in increasing k (C.R), then the xor butterfly.
   const int gw = blockIdx.x * nwarps + warp;
+  if (gw >= total || (gw < total && (gw / BN == 0 ? p.W0 : p.W1) == nullptr))
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // warps without a logit still order after it
   if (gw < total) {
     const int m = gw / BN;
     const int rem = gw - m * BN;
@@ -172,10 +182,15 @@ __global__ void __launch_bounds__(256, CPL <= 8 ? 2 : 1) k1_router(RouterParams 
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
         const int c = lane + 32 * q;
-        if (c < n_chunks) {
-          wr[q] = __ldg(wv + c);
-          hr[q] = __ldg(hv + c);
-        }
+        if (c < n_chunks) wr[q] = __ldg(wv + c);
+      }
+      // programmatic dependent launch: the router weights do not depend on the previous kernel
+      // (the layer before's final K2), h does -- wait for that grid only now (no-op otherwise)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int c = lane + 32 * q;
+        if (c < n_chunks) hr[q] = __ldg(hv + c);
       }
       double acc = 0.0;
 #pragma unroll
@@ -260,8 +275,8 @@ __global__ void __launch_bounds__(256, CPL <= 8 ? 2 : 1) k1_router(RouterParams 
     __syncthreads();
     const unsigned long long tag = (unsigned long long)p.seq << 32;
     for (int i = threadIdx.x; i < p.B * p.K; i += blockDim.x) {   // coalesced PCIe bursts
-      p.mb_ids[i] = tag | (uint32_t)p.ids[i];
-      p.mb_w[i] = tag | __float_as_uint(p.w[i]);
+      st_wt(p.mb_ids + i, tag | (uint32_t)p.ids[i]);
+      st_wt(p.mb_w + i, tag | __float_as_uint(p.w[i]));
     }
     if (p.dbg && threadIdx.x == 0) p.dbg[3] = gtimer();
   }
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(256, CPL <= 8 ? 2 : 1) k1_router(RouterParams 
     __syncthreads();
     if (p.dbg && threadIdx.x == 0) p.dbg[7] = gtimer();
     const unsigned long long tag = (unsigned long long)p.seq << 32;
-    for (int i = threadIdx.x; i < p.N; i += blockDim.x) p.mb_rank[i] = tag | (uint32_t)p.ranking[i];
+    for (int i = threadIdx.x; i < p.N; i += blockDim.x) st_wt(p.mb_rank + i, tag | (uint32_t)p.ranking[i]);
   }
   if (threadIdx.x == 0) *p.ticket = 0u;
   if (p.dbg && threadIdx.x == 0) p.dbg[4] = gtimer();
@@ -352,8 +367,8 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
         const float wv = (float)(ek / part);
         p.ids[b * p.K + lane] = id;
         p.w[b * p.K + lane] = wv;
-        p.mb_ids[b * p.K + lane] = tag | (uint32_t)id;
-        p.mb_w[b * p.K + lane] = tag | __float_as_uint(wv);
+        st_wt(p.mb_ids + b * p.K + lane, tag | (uint32_t)id);
+        st_wt(p.mb_w + b * p.K + lane, tag | __float_as_uint(wv));
       }
       __syncwarp();
     }
@@ -408,7 +423,7 @@ __global__ void __launch_bounds__(256) k1_select(RouterParams p) {
   }
   __syncthreads();
   for (int i = threadIdx.x; i < p.N; i += blockDim.x) {
-    p.mb_rank[i] = tag | (uint32_t)p.ranking[i];
+    st_wt(p.mb_rank + i, tag | (uint32_t)p.ranking[i]);
     p.sel_cnt[i] = 0;
     p.sel_max[i] = 0ull;
   }
@@ -425,11 +440,20 @@ cudaError_t router_init() {
   return e != cudaSuccess ? e : f != cudaSuccess ? f : g;
 }
 
-void launch_router(const RouterParams& p, cudaStream_t s) {
+void launch_router(const RouterParams& p, cudaStream_t s, bool pdl) {
   const int warps = 2 * p.B * p.N;
   const int grid = (warps + 7) / 8;
-  if (p.d > 2048) k1_router<16><<<grid, 256, 0, s>>>(p);
-  else k1_router<8><<<grid, 256, 0, s>>>(p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (p.d > 2048) cudaLaunchKernelEx(&cfg, k1_router<16>, p);
+  else cudaLaunchKernelEx(&cfg, k1_router<8>, p);
   if (p.B > kRouterSplitB) k1_select<<<(p.B + 7) / 8, 256, 0, s>>>(p);
 }
 

@@ -358,6 +358,8 @@ struct moepic_ctx {
   uint8_t* mailbox = nullptr;        // mapped pinned
   uint8_t* mailbox_dev = nullptr;
   cudaStream_t copy = nullptr;
+  cudaStream_t copy2 = nullptr;      // second on-demand copy stream (MOEPIC_COPY_STREAMS=2)
+  cudaEvent_t ev_copy2 = nullptr;
   cudaEvent_t ev_od = nullptr, ev_od_head = nullptr, ev_plan[2] = {nullptr, nullptr}, ev_step[2] = {nullptr, nullptr};
   bool ev_step_rec[2] = {false, false};
   cudaEvent_t ev_tmp = nullptr;
@@ -398,6 +400,58 @@ struct moepic_ctx {
   // decode: the step's last on-demand copy is split so its final tail_bytes land last; the K2
   // launch over everything else runs while the tail is still in flight (0 disables)
   size_t od_tail_bytes = 64ull << 20;
+  // decode: a step whose last on-demand copy is too small to split makes that whole copy the tail
+  // (MOEPIC_OD_SPLIT_BOUNDARY=0 turns this off)
+  bool od_split_boundary = true;
+  // MOEPIC_TIMELINE=<path> (tools): per decode layer step, %globaltimer stamps of the router, the
+  // K2 launches before the final one, the final (combining) K2 and the completion of the step's
+  // last on-demand copy (a one-thread kernel on the copy stream), plus host stamps of the call,
+  // routing seen, first / last copy issued and return, converted to GPU time; JSON lines at destroy
+  std::string tl_path;
+  unsigned long long* tl_dev = nullptr;   // [kProfRing] starts | [kProfRing] ends (stamp_start/end)
+  int64_t tl_off0 = 0, tl_h0 = 0;         // GPU ns - host steady_clock ns at host time tl_h0 (create)
+  // clock offset by handshake over mapped host memory: the kernel announces itself, the host reads
+  // its clock and releases it, the kernel stamps %globaltimer when it sees the release (one PCIe
+  // read latency, ~1 us, after the host stamp); best of 10.  %globaltimer drifts against the host
+  // clock by tens of ppm, so the dump re-calibrates and interpolates linearly.
+  void tl_calibrate(int64_t& host_ns, int64_t& off) {
+    auto* hv = reinterpret_cast<volatile unsigned long long*>(scratch_h);
+    int64_t best = INT64_MAX;
+    for (int it = 0; it < 10; ++it) {
+      hv[0] = hv[1] = hv[2] = 0;
+      launch_clock_sync(reinterpret_cast<unsigned long long*>(scratch_d), nullptr);
+      while (hv[0] == 0) {
+      }
+      const auto a = std::chrono::steady_clock::now();
+      hv[2] = 1;
+      while (hv[1] == 0) {
+      }
+      const auto b = std::chrono::steady_clock::now();
+      const int64_t ha = std::chrono::duration_cast<std::chrono::nanoseconds>(a.time_since_epoch()).count();
+      const int64_t hb = std::chrono::duration_cast<std::chrono::nanoseconds>(b.time_since_epoch()).count();
+      if (hb - ha < best) {
+        best = hb - ha;
+        host_ns = (ha + hb) / 2;
+        off = (int64_t)hv[1] - host_ns;
+      }
+    }
+    cudaDeviceSynchronize();
+  }
+  int tl_rec = -1;
+  int64_t tl_skip = 0, tl_seen = 0;       // MOEPIC_TIMELINE_SKIP: layer steps before recording starts
+  struct TlHost {
+    int layer;
+    int64_t t[5];
+    uint64_t od_bytes;
+  };
+  std::vector<TlHost> tl_host;
+  static constexpr int kTlMax = kProfRing / 4;
+  unsigned long long* tl_slot(int k) const {
+    return (tl_dev && tl_rec >= 0 && tl_rec < kTlMax) ? tl_dev + (size_t)tl_rec * 4 + k : nullptr;
+  }
+  // the decode router is launched as a programmatic dependent of the previous kernel on the
+  // stream (MOEPIC_PDL=0 turns this off)
+  bool pdl = true;
   size_t kFeedDepth = 3;
   static constexpr int kFeedRing = 16;
   bool cancel_prefetch = true;
@@ -604,6 +658,14 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->mailbox_dev), ctx->mailbox, 0) != cudaSuccess)
     return bail(MOEPIC_ERUNTIME);
   if (cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
+  {
+    const char* e = getenv("MOEPIC_COPY_STREAMS");
+    if (!e || atoi(e) >= 2) {
+      if (cudaStreamCreateWithFlags(&ctx->copy2, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_copy2, cudaEventDisableTiming) != cudaSuccess)
+        return bail(MOEPIC_ERUNTIME);
+    }
+  }
   cudaEvent_t* evs[] = {&ctx->ev_od, &ctx->ev_od_head, &ctx->ev_plan[0], &ctx->ev_plan[1], &ctx->ev_step[0], &ctx->ev_step[1],
                         &ctx->ev_tmp};
   for (auto* e : evs)
@@ -616,6 +678,18 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;
   if (const char* e = getenv("MOEPIC_OD_TAIL_MB")) ctx->od_tail_bytes = (size_t)atol(e) << 20;
   if (const char* e = getenv("MOEPIC_OD_TAIL_KB")) ctx->od_tail_bytes = (size_t)atol(e) << 10;   // tests: small shapes
+  if (const char* e = getenv("MOEPIC_OD_SPLIT_BOUNDARY")) ctx->od_split_boundary = atoi(e) != 0;
+  if (const char* e = getenv("MOEPIC_PDL")) ctx->pdl = atoi(e) != 0;
+  if (const char* e = getenv("MOEPIC_TIMELINE")) {
+    ctx->tl_path = e;
+    if (const char* k = getenv("MOEPIC_TIMELINE_SKIP")) ctx->tl_skip = atol(k);
+    if (cudaMalloc(&ctx->tl_dev, (size_t)2 * kProfRing * 8) != cudaSuccess ||
+        cudaMemset(ctx->tl_dev, 0xFF, (size_t)kProfRing * 8) != cudaSuccess ||
+        cudaMemset(ctx->tl_dev + kProfRing, 0, (size_t)kProfRing * 8) != cudaSuccess)
+      return bail(MOEPIC_ERUNTIME);
+    ctx->tl_calibrate(ctx->tl_h0, ctx->tl_off0);
+    cudaDeviceSynchronize();
+  }
   if (const char* e = getenv("MOEPIC_FEED_DEPTH")) ctx->kFeedDepth = (size_t)std::min(atol(e), (long)moepic_ctx::kFeedRing);
   if (const char* e = getenv("MOEPIC_PF_CTA_PAIR")) ctx->pf_cta_pair = atoi(e) ? 1 : 0;
   if (const char* e = getenv("MOEPIC_K2T_MODE")) ctx->k2t_mode = atoi(e);
@@ -812,7 +886,9 @@ moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg, 
   std::string e = ctx->cp->configure(to_params(cfg, ctx->desc.L), ctx->lay.pool_rows);
   if (!e.empty()) return fail(&ctx->err, MOEPIC_EINVAL, "%s", e.c_str());
   // re-layout: per-layer slot regions, tops of cached experts H2D
-  if (ctx->poison) CK(cudaMemset(ctx->arena + ctx->lay.pool, 0xFF, ctx->lay.pool_rows * ctx->rb()));
+  // (poison: on the copy stream, ordered before the top copies -- a legacy-stream cudaMemset is
+  // not ordered against the non-blocking copy stream and could land after them)
+  if (ctx->poison) CK(cudaMemsetAsync(ctx->arena + ctx->lay.pool, 0xFF, ctx->lay.pool_rows * ctx->rb(), ctx->copy));
   uint64_t off = 0;
   const uint64_t rb = ctx->rb();
   for (int i = 0; i < ctx->desc.L; ++i) {
@@ -898,7 +974,7 @@ static moepic_status launch_group_tc(moepic_ctx* ctx, const std::vector<StepSeg>
     comb.push_back(CombineSeg{ws_next, G, (uint32_t)((1ull << B) - 1)});
     ws_next += (int64_t)G * B * d;
     const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
-    kp.tstamp = ctx->tstamp(pe);
+    kp.tstamp = ctx->tl_slot(3) ? ctx->tl_slot(3) : ctx->tstamp(pe);
     static unsigned long long* dbg_buf = nullptr;   // MOEPIC_K2_TRACE: per-CTA phases to stderr (tools)
     kp.dbg = nullptr;
     if (ctx->k2_trace) {
@@ -1036,7 +1112,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       fuse->done = true;
     }
     const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_EXPERT);
-    kp.tstamp = ctx->tstamp(pe);
+    kp.tstamp = ctx->tl_slot(kp.combine ? 1 : 3) ? ctx->tl_slot(kp.combine ? 1 : 3) : ctx->tstamp(pe);
     kp.dbg = nullptr;
     static unsigned long long* dbg_buf = nullptr;   // MOEPIC_K2_TRACE: phase spans to stderr (tools)
     const bool trace = ctx->k2_trace;
@@ -1149,7 +1225,7 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
   rp.seq = ++ctx->seq;
   rp.B = B; rp.d = d.d; rp.N = d.N; rp.K = d.K; rp.renorm = d.renorm_topk;
   const int pe = ctx->prof_begin(s, MOEPIC_KERNEL_ROUTER);
-  rp.tstamp = ctx->tstamp(pe);
+  rp.tstamp = ctx->tl_slot(0) ? ctx->tl_slot(0) : ctx->tstamp(pe);
   rp.dbg = nullptr;
   if (ctx->k1_trace) {   // phase stamps per launch (tools): ring of 4096 x 8 u64
     if (!ctx->k1dbg) {
@@ -1161,7 +1237,7 @@ static moepic_status run_router(moepic_ctx* ctx, const uint16_t* h, int B, int l
     cudaMemsetAsync(rp.dbg + 1, 0, 56, s);
     ctx->k1dbg_n++;
   }
-  launch_router(rp, s);
+  launch_router(rp, s, ctx->pdl && read_ids && !ctx->k1_trace);
   ctx->prof_end(pe, s, (uint64_t)((rp.W0 ? 1 : 0) + (rp.W1 ? 1 : 0)) * d.N * d.d * 2 + (uint64_t)B * d.d * 2);
   CK(cudaGetLastError());
   ctx->ctr.kernel_launches += B > kRouterSplitB ? 2 : 1;
@@ -1489,6 +1565,12 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
 
   // ---- K1 (router + fused next-layer predictor) and the mailbox handoff
   const auto t_call = std::chrono::steady_clock::now();
+  ctx->tl_rec = -1;
+  if (ctx->tl_dev && B <= kDecodeMaxB && ctx->tl_seen++ >= ctx->tl_skip &&
+      (int)ctx->tl_host.size() < moepic_ctx::kTlMax) {
+    ctx->tl_rec = (int)ctx->tl_host.size();
+    ctx->tl_host.push_back(moepic_ctx::TlHost{layer, {0, 0, 0, 0, 0}, 0});
+  }
   moepic_status st = MOEPIC_OK;
   const bool route_here = cp_ids == nullptr;
   if (route_here) {
@@ -1498,7 +1580,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     cp_B = B;
   }
   const auto t_routed = std::chrono::steady_clock::now();
-  auto t_first_copy = t_routed;   // MOEPIC_HOST_TIMING
+  auto t_first_copy = t_routed;   // MOEPIC_HOST_TIMING / MOEPIC_TIMELINE
   if (st != MOEPIC_OK) return st;
 
   // ---- control plane (classification, counters, admission)
@@ -1548,23 +1630,62 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   const bool split_ok = B <= kDecodeMaxB && ctx->od_tail_bytes > 0;
   const int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
   const uint8_t* split_dst = nullptr;   // segment whose tail was split off
+  bool split_whole = false;             // ... or which is the tail as a whole (ev_od_head before it)
+  // Two copy streams (MOEPIC_COPY_STREAMS=2, default): the step's on-demand copies alternate
+  // between them, so one DMA engine's per-copy start-up overlaps the other's transfer (many
+  // 2-10 MB bottoms per layer on Qwen3 / DeepSeek: MOEPIC_TIMELINE measured ~40 us per layer from
+  // the first cudaMemcpyAsync to the link running at rate with one stream).  The step's last copy
+  // always goes to ctx->copy, which first waits for the other stream, so ev_od / ev_od_head keep
+  // their meaning and the prefetch feed (ctx->copy) still follows every on-demand byte.
+  bool used2 = false;
+  auto join2 = [&]() -> moepic_status {   // ctx->copy waits for everything issued on copy2 so far
+    if (!used2) return MOEPIC_OK;
+    CK(cudaEventRecord(ctx->ev_copy2, ctx->copy2));
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_copy2, 0));
+    used2 = false;
+    return MOEPIC_OK;
+  };
   auto copy = [&](uint8_t* dst, const uint8_t* src, int32_t rows, bool evicted = false) -> moepic_status {
     const size_t bytes = (size_t)rows * rb;
     const auto tw0 = std::chrono::steady_clock::now();
     if (!waited) {   // the buffers / slots written here were last read by earlier steps
       for (int b2 = 0; b2 < 2; ++b2)
-        if (ctx->ev_step_rec[b2]) CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[b2], 0));
+        if (ctx->ev_step_rec[b2]) {
+          CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_step[b2], 0));
+          if (ctx->copy2) CK(cudaStreamWaitEvent(ctx->copy2, ctx->ev_step[b2], 0));
+        }
       waited = true;
     }
     const auto tw1 = std::chrono::steady_clock::now();
-    if (evicted && ctx->poison) CK(cudaMemsetAsync(dst, 0xFF, bytes, ctx->copy));   // the victim's old top
-    if (split_ok && n_od == n_copies - 1 && (int64_t)rows > 2 * tail_rows_split) {
+    const bool last = n_od == n_copies - 1;
+    cudaStream_t cs = ctx->copy;
+    if (ctx->copy2 && !last && (n_od & 1)) {
+      cs = ctx->copy2;
+      used2 = true;
+    }
+    if (evicted && ctx->poison) CK(cudaMemsetAsync(dst, 0xFF, bytes, cs));   // the victim's old top
+    if (cs != ctx->copy) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs));
+      ctx->ctr.h2d_copies++;
+    } else if (split_ok && last && (int64_t)rows > 2 * tail_rows_split) {
+      moepic_status st2 = join2();
+      if (st2 != MOEPIC_OK) return st2;
       const size_t head = bytes - (size_t)tail_rows_split * rb;
       CK(cudaMemcpyAsync(dst, src, head, cudaMemcpyHostToDevice, ctx->copy));
       CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
       CK(cudaMemcpyAsync(dst + head, src + head, bytes - head, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies += 2;
       split_dst = dst;
+    } else if (split_ok && ctx->od_split_boundary && last && n_copies >= 2) {
+      // a small last copy is the tail as a whole: the K2 launch over everything else waits for
+      // the copies before it, so only the last copy's rows remain after the link goes quiet
+      moepic_status st2 = join2();
+      if (st2 != MOEPIC_OK) return st2;
+      CK(cudaEventRecord(ctx->ev_od_head, ctx->copy));
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
+      ctx->ctr.h2d_copies++;
+      split_dst = dst;
+      split_whole = true;
     } else {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies++;
@@ -1574,7 +1695,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
       ctx->hc[1] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw1).count();
       ctx->hc_n++;
     }
-    if (n_od++ == 0 && ctx->host_timing) t_first_copy = std::chrono::steady_clock::now();
+    if (n_od++ == 0 && (ctx->host_timing || ctx->tl_rec >= 0)) t_first_copy = std::chrono::steady_clock::now();
     return MOEPIC_OK;
   };
   const uint32_t all_tok = B >= 32 ? 0xFFFFFFFFu : ((1u << B) - 1u);
@@ -1649,14 +1770,20 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     StepSeg& last = gC.back();
     if (last.base != split_dst || n_od != n_copies)
       return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: split copy is not the step's last on-demand segment");
-    StepSeg tail = last;
-    last.nrows -= (int32_t)tail_rows_split;
-    tail.base = split_dst + (size_t)last.nrows * rb;
-    tail.nrows = (int32_t)tail_rows_split;
-    tail.row0 = last.row0 + last.nrows;
-    gC.push_back(tail);
-    tail_base = tail.base;
+    if (split_whole) {
+      tail_base = split_dst;
+    } else {
+      StepSeg tail = last;
+      last.nrows -= (int32_t)tail_rows_split;
+      tail.base = split_dst + (size_t)last.nrows * rb;
+      tail.nrows = (int32_t)tail_rows_split;
+      tail.row0 = last.row0 + last.nrows;
+      gC.push_back(tail);
+      tail_base = tail.base;
+    }
   }
+  if ((st = join2()) != MOEPIC_OK) return st;
+  if (n_od && ctx->tl_slot(2)) launch_stamp(ctx->tl_slot(2), ctx->copy);
   if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
   {   // an expert's on-demand segments consecutive, tops first (the prefill down GEMM groups by expert)
     std::vector<int32_t> pos(d.N, 0);
@@ -1766,6 +1893,18 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     ctx->pending = next;
   }
 
+  if (ctx->tl_rec >= 0) {
+    auto ns = [&](std::chrono::steady_clock::time_point t) {   // raw host ns: converted at the dump
+      return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t.time_since_epoch()).count();
+    };
+    auto& hr = ctx->tl_host[ctx->tl_rec];
+    hr.t[0] = ns(t_call);
+    hr.t[1] = ns(t_routed);
+    hr.t[2] = n_od ? ns(t_first_copy) : 0;
+    hr.t[3] = ns(t_copies);
+    hr.t[4] = ns(std::chrono::steady_clock::now());
+    hr.od_bytes = res.pcie_ondemand;
+  }
   if (ctx->host_timing) {   // MOEPIC_HOST_TIMING (tools): host-side phases of the call, us
     const auto t_end = std::chrono::steady_clock::now();
     auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -2336,6 +2475,31 @@ const char* moepic_last_error(const moepic_ctx* ctx) { return ctx ? ctx->err.c_s
 void moepic_destroy(moepic_ctx* ctx) {
   if (!ctx) return;
   cudaDeviceSynchronize();
+  if (ctx->tl_dev && !ctx->tl_host.empty()) {   // MOEPIC_TIMELINE
+    int64_t h1 = 0, off1 = 0;
+    ctx->tl_calibrate(h1, off1);
+    auto conv = [&](int64_t h) -> long long {
+      if (h == 0) return 0;
+      const double f = h1 > ctx->tl_h0 ? (double)(h - ctx->tl_h0) / (double)(h1 - ctx->tl_h0) : 0.0;
+      return (long long)(h + ctx->tl_off0 + (int64_t)((double)(off1 - ctx->tl_off0) * f));
+    };
+    std::vector<unsigned long long> g((size_t)2 * kProfRing);
+    cudaMemcpy(g.data(), ctx->tl_dev, g.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(ctx->tl_path.c_str(), "w")) {
+      auto st = [&](size_t i) { return g[i] == ~0ull ? -1LL : (long long)g[i]; };
+      auto en = [&](size_t i) { return g[kProfRing + i] == 0 ? -1LL : (long long)g[kProfRing + i]; };
+      for (size_t r = 0; r < ctx->tl_host.size(); ++r) {
+        const auto& h = ctx->tl_host[r];
+        fprintf(f, "{\"rec\": %zu, \"layer\": %d, \"host\": [%lld, %lld, %lld, %lld, %lld], \"od_bytes\": %llu, "
+                "\"router\": [%lld, %lld], \"k2_first\": [%lld, %lld], \"k2_final\": [%lld, %lld], \"copy_done\": %lld}\n",
+                r, h.layer, conv(h.t[0]), conv(h.t[1]), conv(h.t[2]), conv(h.t[3]), conv(h.t[4]),
+                (unsigned long long)h.od_bytes, st(r * 4), en(r * 4), st(r * 4 + 3), en(r * 4 + 3), st(r * 4 + 1),
+                en(r * 4 + 1), st(r * 4 + 2));
+      }
+      fclose(f);
+    }
+  }
+  if (ctx->tl_dev) cudaFree(ctx->tl_dev);
   if (ctx->ht_n)
     fprintf(stderr, "[hosttiming] %llu calls: launch router + wait routing %.1f | routing -> first copy issued %.1f | "
             "routing -> all copies issued %.1f | K2 launches + next plan %.1f us\n", (unsigned long long)ctx->ht_n,
@@ -2382,6 +2546,8 @@ void moepic_destroy(moepic_ctx* ctx) {
     if (g.idx_h) cudaFreeHost(g.idx_h);
   }
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->copy2) cudaStreamDestroy(ctx->copy2);
+  if (ctx->ev_copy2) cudaEventDestroy(ctx->ev_copy2);
   for (auto e : ctx->feed_ev)
     if (e) cudaEventDestroy(e);
   for (auto& pe : ctx->prof) {

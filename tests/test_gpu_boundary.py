@@ -221,10 +221,12 @@ def test_poison_mode_parity_unchanged():
     evicted slots NaN-filled): a stale or early read would surface as NaN."""
     sel = ("test_toy_full_replay or test_split_identity_every_mode or test_policies_replay_qwen_small "
            "or test_od_tail_split or test_cancel_prefetch or test_prefill_smallest_batches "
-           "or test_configure_drops_pending_prefetch or test_decode_max_batch_32")
+           "or test_configure_drops_pending_prefetch or test_decode_max_batch_32 or test_deepseek_shape "
+           "or test_window_cut_prefetch or test_k2t or test_q4_prefill_parity")
     env = dict(os.environ, MOEPIC_POISON="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
-                        "tests/test_gpu_parity.py", "tests/test_gpu_edges.py"],
+                        "tests/test_gpu_parity.py", "tests/test_gpu_edges.py", "tests/test_gpu_k2t.py",
+                        "tests/test_gpu_q4.py"],
                        env=env, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
