@@ -445,9 +445,9 @@ struct moepic_ctx {
     uint64_t od_bytes;
   };
   std::vector<TlHost> tl_host;
-  static constexpr int kTlMax = kProfRing / 4;
+  static constexpr int kTlMax = kProfRing / 8;
   unsigned long long* tl_slot(int k) const {
-    return (tl_dev && tl_rec >= 0 && tl_rec < kTlMax) ? tl_dev + (size_t)tl_rec * 4 + k : nullptr;
+    return (tl_dev && tl_rec >= 0 && tl_rec < kTlMax) ? tl_dev + (size_t)tl_rec * 8 + k : nullptr;
   }
   // the decode router is launched as a programmatic dependent of the previous kernel on the
   // stream (MOEPIC_PDL=0 turns this off)
@@ -659,8 +659,8 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
     return bail(MOEPIC_ERUNTIME);
   if (cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess) return bail(MOEPIC_ERUNTIME);
   {
-    const char* e = getenv("MOEPIC_COPY_STREAMS");
-    if (!e || atoi(e) >= 2) {
+    const char* e = getenv("MOEPIC_COPY_STREAMS");   // default 1: two streams measured neutral
+    if (e && atoi(e) >= 2) {
       if (cudaStreamCreateWithFlags(&ctx->copy2, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_copy2, cudaEventDisableTiming) != cudaSuccess)
         return bail(MOEPIC_ERUNTIME);
@@ -1631,12 +1631,13 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   const int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
   const uint8_t* split_dst = nullptr;   // segment whose tail was split off
   bool split_whole = false;             // ... or which is the tail as a whole (ev_od_head before it)
-  // Two copy streams (MOEPIC_COPY_STREAMS=2, default): the step's on-demand copies alternate
+  // Two copy streams (MOEPIC_COPY_STREAMS=2; default 1): the step's on-demand copies alternate
   // between them, so one DMA engine's per-copy start-up overlaps the other's transfer (many
   // 2-10 MB bottoms per layer on Qwen3 / DeepSeek: MOEPIC_TIMELINE measured ~40 us per layer from
   // the first cudaMemcpyAsync to the link running at rate with one stream).  The step's last copy
   // always goes to ctx->copy, which first waits for the other stream, so ev_od / ev_od_head keep
-  // their meaning and the prefetch feed (ctx->copy) still follows every on-demand byte.
+  // their meaning and the prefetch feed (ctx->copy) still follows every on-demand byte.  Measured
+  // neutral (Qwen3 32.48 vs 32.52, DeepSeek 46.34 vs 46.50 tokens/s): the start-up is not per copy.
   bool used2 = false;
   auto join2 = [&]() -> moepic_status {   // ctx->copy waits for everything issued on copy2 so far
     if (!used2) return MOEPIC_OK;
@@ -1658,6 +1659,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     }
     const auto tw1 = std::chrono::steady_clock::now();
     const bool last = n_od == n_copies - 1;
+    if (n_od == 0 && ctx->tl_slot(4)) launch_stamp(ctx->tl_slot(4), ctx->copy);   // MOEPIC_TIMELINE
     cudaStream_t cs = ctx->copy;
     if (ctx->copy2 && !last && (n_od & 1)) {
       cs = ctx->copy2;
@@ -2491,10 +2493,11 @@ void moepic_destroy(moepic_ctx* ctx) {
       for (size_t r = 0; r < ctx->tl_host.size(); ++r) {
         const auto& h = ctx->tl_host[r];
         fprintf(f, "{\"rec\": %zu, \"layer\": %d, \"host\": [%lld, %lld, %lld, %lld, %lld], \"od_bytes\": %llu, "
-                "\"router\": [%lld, %lld], \"k2_first\": [%lld, %lld], \"k2_final\": [%lld, %lld], \"copy_done\": %lld}\n",
+                "\"router\": [%lld, %lld], \"k2_first\": [%lld, %lld], \"k2_final\": [%lld, %lld], \"copy_done\": %lld, "
+                "\"copy_start\": %lld}\n",
                 r, h.layer, conv(h.t[0]), conv(h.t[1]), conv(h.t[2]), conv(h.t[3]), conv(h.t[4]),
-                (unsigned long long)h.od_bytes, st(r * 4), en(r * 4), st(r * 4 + 3), en(r * 4 + 3), st(r * 4 + 1),
-                en(r * 4 + 1), st(r * 4 + 2));
+                (unsigned long long)h.od_bytes, st(r * 8), en(r * 8), st(r * 8 + 3), en(r * 8 + 3), st(r * 8 + 1),
+                en(r * 8 + 1), st(r * 8 + 2), st(r * 8 + 4));
       }
       fclose(f);
     }

@@ -10,6 +10,8 @@ For consecutive decode layer steps i -> i+1 (times in microseconds, medians over
   router(i+1)                         in-kernel span
   router start -> host sees routing   (router up to the routing words + mailbox poll)
   routing seen -> first copy issued   host classification / plan bookkeeping
+  first copy issued -> copy stream    a one-thread stamp kernel on the copy stream right before the
+                                      first on-demand copy: when the stream gets to the copies
   first copy issued -> first byte     estimated: copy_done(i+1) - od_bytes(i+1) / link rate
   link idle                           first byte(i+1) - copy_done(i)
 """
@@ -26,7 +28,7 @@ def main():
     a = ap.parse_args()
     recs = [json.loads(x) for x in open(a.path) if x.strip()][a.skip:]
     rows = {k: [] for k in ("wait_k2", "k2_final", "k2_to_router", "router", "router_to_seen", "seen_to_issue",
-                            "issue_to_byte", "link_idle", "od_us")}
+                            "issue_to_copy_stream", "copy_stream_to_byte", "issue_to_byte", "link_idle", "od_us")}
     for r, n in zip(recs, recs[1:]):
         cd, fs, fe = r["copy_done"], r["k2_final"][0], r["k2_final"][1]
         rs, re_ = n["router"]
@@ -43,6 +45,9 @@ def main():
         rows["router_to_seen"].append((seen - rs) / 1e3)
         rows["seen_to_issue"].append((first_issue - seen) / 1e3)
         rows["issue_to_byte"].append((first_byte - first_issue) / 1e3)
+        if n.get("copy_start", -1) > 0:
+            rows["issue_to_copy_stream"].append((n["copy_start"] - first_issue) / 1e3)
+            rows["copy_stream_to_byte"].append((first_byte - n["copy_start"]) / 1e3)
         rows["link_idle"].append((first_byte - cd) / 1e3)
         rows["od_us"].append(od_us)
     print(f"{len(rows['link_idle'])} layer transitions")
