@@ -1393,14 +1393,15 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
   // gate/up runs on CTA pairs (UMMA M = 256: half the B operand bytes per SM; ncu: tensor pipe
   // 88% vs 75% for single CTAs) unless rounding the experts' 128-row tiles up to pairs would
   // waste more than 1/10 of the MMA work (few tokens per expert, e.g. Qwen3-shaped prefill).
-  // down keeps single CTAs (90% vs 84%: its B tile is already shared by both MMAs, hi and lo).
   int64_t mt1 = 0, mt2 = 0;
   for (int e = 0; e < NE; ++e) {
     mt1 += table[e].mtiles;
     mt2 += 2 * ((table[e].mtiles + 1) / 2);
   }
   const int CGu = ctx->pf_cta_pair >= 0 ? (ctx->pf_cta_pair ? 2 : 1) : (mt2 * 10 <= mt1 * 11 ? 2 : 1);
-  const int CGd = ctx->pf_cta_pair >= 0 ? (ctx->pf_cta_pair ? 2 : 1) : 1;
+  // down follows the same choice since its activation is one fp16 operand (reading Q31): with the
+  // bf16 hi / lo pair a single CTA's B tile fed two MMAs and pairs did not pay (90 % vs 84 %)
+  const int CGd = ctx->pf_cta_pair >= 0 ? (ctx->pf_cta_pair ? 2 : 1) : CGu;
   auto ptiles = [&](int e, int CG) { return (int64_t)((table[e].mtiles + CG - 1) / CG); };
 
   auto run_group = [&](const std::vector<StepSeg>& g0) -> moepic_status {
