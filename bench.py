@@ -351,7 +351,8 @@ def run_ours(args, log):
         if cal_tokens:
             # the prefetch window of this stack (P:389 / P:412 T_wind, reading Q30): with no
             # attention block the link idles per layer for the serial chain final K2 -> router ->
-            # host -> first copy.  Measured as (layer time - PCIe bytes / link rate) over the last
+            # host -> first copy (profiles/r02_decode_chain_timeline.md).  Measured as (layer
+            # time - PCIe bytes / link rate) over the last
             # cal_tokens adaptation tokens (no timing events), rounded to 10 us so the configuration
             # reproduces run to run; the plan of every layer is cut at that many rows of link time.
             # It is not fed back into Alg. 1 as T_att: re-solving with it moved DeepSeek to smaller
@@ -367,7 +368,10 @@ def run_ours(args, log):
             lay_ms = a0.elapsed_time(a1) / (cal_tokens * L)
             link_ms = (cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] - cc0["pcie_ondemand_bytes"]
                        - cc0["pcie_prefetch_bytes"]) / (cal_tokens * L) / (ALG1_PCIE_GBS * 1e9) * 1e3
-            window_us = max(0.0, round((lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
+            # three quarters of it: the next layer's on-demand copies queue behind the prefetch (one
+            # FIFO copy stream), so the window leaves their DMA start-up its own margin (measured:
+            # the full idle moved DeepSeek -3.3 %, three quarters +0.8 %; Qwen3 +3.4 % / +1.6 %)
+            window_us = max(0.0, round(0.75 * (lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
             window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
             base_cfg["prefetch_rows_i"] = [window_rows] * L
             log(f"[bench] link-idle window {window_us:.0f} us per layer ({window_rows} rows)")
