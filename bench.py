@@ -372,6 +372,10 @@ def run_ours(args, log):
             # FIFO copy stream), so the window leaves their DMA start-up its own margin (measured:
             # the full idle moved DeepSeek -3.3 %, three quarters +0.8 %; Qwen3 +3.4 % / +1.6 %)
             window_us = max(0.0, round(0.75 * (lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
+            if dist:   # one window for the whole group (rank 0's), so every rank plans alike
+                wt = torch.tensor([window_us], device="cuda")
+                dist.broadcast(wt, 0)
+                window_us = float(wt.item())
             window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
             base_cfg["prefetch_rows_i"] = [window_rows] * L
             log(f"[bench] link-idle window {window_us:.0f} us per layer ({window_rows} rows)")
@@ -741,8 +745,8 @@ def main():
     ap.add_argument("--y-cap", type=int, default=None, help="prefetch count cap per layer (default K*B)")
     ap.add_argument("--prefetch-window-us", default="auto",
                     help="reading Q30: cut each layer's prefetch plan at this many microseconds of link time; "
-                         "auto (adaptive decode configs) = the measured per-layer link-idle time, also Alg. 1's "
-                         "T_att; 0 = no window (Alg. 1's Y caps the plan)")
+                         "auto (adaptive decode configs) = 0.75 x the measured per-layer link-idle time; "
+                         "0 = no window (Alg. 1's Y caps the plan)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.e2e_steps is None:
