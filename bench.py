@@ -240,7 +240,6 @@ def run_ours(args, log):
     window_rows = None
     window_us = None
     rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
-    auto_window = args.prefetch_window_us == "auto" and cfg.get("adaptive") and not cfg.get("prefill")
     if args.prefetch_window_us not in ("auto", "0", "0.0"):   # reading Q30: a fixed window per layer
         window_us = float(args.prefetch_window_us)
         window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
@@ -255,6 +254,8 @@ def run_ours(args, log):
         base_cfg["v_e"] = mode["v_e"]
     if mode.get("adaptive") is False:
         cfg["adaptive"] = False
+    # reading Q30: the measured window applies to every decode mode that prefetches
+    auto_window = args.prefetch_window_us == "auto" and base_cfg.get("prefetch", 1) and not cfg.get("prefill")
     ctx.configure(**base_cfg)
     log(f"[bench] configure (re-layout {v_e:.0f} tops) {time.time() - t0:.1f}s")
     transport = None
@@ -263,9 +264,9 @@ def run_ours(args, log):
         ctx.join_process_group(api.M.TRANSPORT_NCCL if transport == "nccl" else api.M.TRANSPORT_PEER)
         log(f"[bench] rank {rank} joined the {parallel} group ({transport} transport)")
     adapt_tokens = 2 * args.tau if cfg.get("adaptive") else 0
-    cal_tokens = 8 if auto_window else 0   # link-idle calibration after Alg. 1 (reading Q30)
-    adapt_tokens += cal_tokens
-    T = adapt_tokens + args.warmup + args.steps
+    cal_tokens = 8 if auto_window else 0   # link-idle calibration before Alg. 1 (reading Q30)
+    pre_tokens = adapt_tokens + cal_tokens
+    T = pre_tokens + args.warmup + args.steps
     # token t, layer i uses rows [t*B, (t+1)*B) of a [T*B][L][d] organic hidden-state process
     # stored [L][tokens][d] so every per-layer batch slice is a contiguous [B][d] block
     H = synth.hidden_states(1, (T + args.e2e_steps + 1) * B, L, S.d).permute(1, 0, 2).contiguous().to("cuda")
@@ -334,60 +335,60 @@ def run_ours(args, log):
         # Alg. 1 outer loop: run 2 tau tokens on the uniform theta = 0.5 layout, profile
         # T_moe on this GPU and T_load^exp = U_e / PCIe, then reconfigure with the solver.
         ctx.profile(True)
-        for t in range(adapt_tokens - cal_tokens):
+        for t in range(adapt_tokens):
             step(t)
         torch.cuda.synchronize()
         k2w = ctx.profile_read(api.M.KERNEL_EXPERT)
         ctx.profile(False)
-        rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
         U_e = rbytes * (S.I // world if parallel == "tp" else S.I)   # bytes of one (local) expert
-        t_moe_measured = k2w["total_ms"] / ((adapt_tokens - cal_tokens) * L)   # ms of expert compute per layer-step
+        t_moe_measured = k2w["total_ms"] / (adapt_tokens * L)       # ms of expert compute per layer-step
         if args.alg1_inputs == "measured":
             t_load = U_e / (pcie * 1e9) * 1e3                      # ms per full expert
             t_moe = t_moe_measured
         else:   # fixed, modelled profile (reproducible run to run): link and HBM rates
             t_load = U_e / (ALG1_PCIE_GBS * 1e9) * 1e3             # of this pool's boxes, K experts'
             t_moe = S.K * B * U_e / (ALG1_HBM_GBS * 1e9) * 1e3 + ALG1_LAUNCH_MS   # rows + launch cost
-        if cal_tokens:
-            # the prefetch window of this stack (P:389 / P:412 T_wind, reading Q30): with no
-            # attention block the link idles per layer for the serial chain final K2 -> router ->
-            # host -> first copy (profiles/r02_decode_chain_timeline.md).  Measured as (layer
-            # time - PCIe bytes / link rate) over the last
-            # cal_tokens adaptation tokens (no timing events), rounded to 10 us so the configuration
-            # reproduces run to run; the plan of every layer is cut at that many rows of link time.
-            # It is not fed back into Alg. 1 as T_att: re-solving with it moved DeepSeek to smaller
-            # theta and lost 3.5 % (Mixtral 0.9 %) against the cut alone (Q30).
-            cc0 = ctx.counters()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            for t in range(adapt_tokens - cal_tokens, adapt_tokens):
-                step(t)
-            a1.record(stream)
-            torch.cuda.synchronize()
-            cc1 = ctx.counters()
-            lay_ms = a0.elapsed_time(a1) / (cal_tokens * L)
-            link_ms = (cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] - cc0["pcie_ondemand_bytes"]
-                       - cc0["pcie_prefetch_bytes"]) / (cal_tokens * L) / (ALG1_PCIE_GBS * 1e9) * 1e3
-            # three quarters of it: the next layer's on-demand copies queue behind the prefetch (one
-            # FIFO copy stream), so the window leaves their DMA start-up its own margin (measured:
-            # the full idle moved DeepSeek -3.3 %, three quarters +0.8 %; Qwen3 +3.4 % / +1.6 %)
-            window_us = max(0.0, round(0.75 * (lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
-            if dist:   # one window for the whole group (rank 0's), so every rank plans alike
-                wt = torch.tensor([window_us], device="cuda")
-                dist.broadcast(wt, 0)
-                window_us = float(wt.item())
-            window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
-            base_cfg["prefetch_rows_i"] = [window_rows] * L
-            log(f"[bench] link-idle window {window_us:.0f} us per layer ({window_rows} rows)")
+    if cal_tokens:
+        # the prefetch window of this stack (P:389 / P:412 T_wind, reading Q30): with no attention
+        # block the link idles per layer for the serial chain final K2 -> router -> host -> first
+        # copy (profiles/r02_decode_chain_timeline.md).  Measured as (layer time - PCIe bytes /
+        # link rate) over cal_tokens tokens (no timing events), rounded to 10 us so the
+        # configuration reproduces run to run; the plan of every layer is cut at that many rows of
+        # link time.  It is not fed back into Alg. 1 as T_att: re-solving with it moved DeepSeek to
+        # smaller theta and lost 3.5 % (Mixtral 0.9 %) against the cut alone (Q30).
+        cc0 = ctx.counters()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for t in range(adapt_tokens, pre_tokens):
+            step(t)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        cc1 = ctx.counters()
+        lay_ms = a0.elapsed_time(a1) / (cal_tokens * L)
+        link_ms = (cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] - cc0["pcie_ondemand_bytes"]
+                   - cc0["pcie_prefetch_bytes"]) / (cal_tokens * L) / (ALG1_PCIE_GBS * 1e9) * 1e3
+        # three quarters of it: the next layer's on-demand copies queue behind the prefetch (one
+        # FIFO copy stream), so the window leaves their DMA start-up its own margin (measured:
+        # the full idle moved DeepSeek -3.3 %, three quarters +0.8 %; Qwen3 +3.4 % / +1.6 %)
+        window_us = max(0.0, round(0.75 * (lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
+        if dist:   # one window for the whole group (rank 0's), so every rank plans alike
+            wt = torch.tensor([window_us], device="cuda")
+            dist.broadcast(wt, 0)
+            window_us = float(wt.item())
+        window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
+        base_cfg["prefetch_rows_i"] = [window_rows] * L
+        log(f"[bench] link-idle window {window_us:.0f} us per layer ({window_rows} rows)")
+        if not adapt_tokens:   # fixed layouts (ablation modes): the same configuration, plus the window
+            ctx.configure(**base_cfg)
+    if adapt_tokens:
         t0 = time.time()
         solved = ctx.configure(use_solver=True, t_att=t_att, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
                                zeta=0.01, **{k: v for k, v in base_cfg.items() if k != "theta_i"})
-        t_att_alg1 = t_att
         alg1_in = {"inputs": args.alg1_inputs, "t_load_exp_ms": round(t_load, 6), "t_moe_ms": round(t_moe, 6),
-                   "t_att_ms": round(t_att_alg1, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
+                   "t_att_ms": round(t_att, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
         log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(solved['theta_eff_i']):.2f}.."
             f"{max(solved['theta_eff_i']):.2f}, C {min(solved['C_i'])}..{max(solved['C_i'])}")
-    for t in range(adapt_tokens, adapt_tokens + args.warmup):
+    for t in range(pre_tokens, pre_tokens + args.warmup):
         step(t)
     torch.cuda.synchronize()
     if dist:
@@ -405,7 +406,7 @@ def run_ours(args, log):
     torch.cuda.synchronize()
     ev0.record(stream)
     per_tok = []
-    for t in range(adapt_tokens + args.warmup, T):
+    for t in range(pre_tokens + args.warmup, T):
         a = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         step(t)
