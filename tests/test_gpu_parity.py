@@ -365,3 +365,65 @@ def test_window_cut_prefetch(B, W, th):
     _replay(m, ctx, orc, toks, api.M.FUSE_PREDICT)
     c = ctx.counters()
     assert c["pred_hits"] > 0 and c["pcie_prefetch_planned_bytes"] > 0
+
+
+@pytest.mark.parametrize("env", [{"MOEPIC_COPY_STREAMS": "2"}, {"MOEPIC_PDL": "0", "MOEPIC_OD_SPLIT_BOUNDARY": "0"}])
+def test_transfer_engine_variants_bit_identical(env, monkeypatch):
+    """The transfer-engine / launch variants change only when things run, never what: traces equal;
+    two copy streams keep the K2 launch grouping, so y is bit-identical; without the PDL router and
+    the boundary split the rows are grouped into launches differently, so y agrees to fp32
+    rounding of the partial sums."""
+    api = _api()
+    S = synth.SHAPES["qwen3"]
+    m = Model(2, S.N, S.K, S.d, S.I, seed=6, gen_device="cuda")
+    H = synth.hidden_states(8, 6, 2, S.d)
+    toks = [[H[t, i][None] for i in range(2)] for t in range(6)]
+    out = []
+    for variant in (None, env):
+        for k in ("MOEPIC_COPY_STREAMS", "MOEPIC_PDL", "MOEPIC_OD_SPLIT_BOUNDARY"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in (variant or {}).items():
+            monkeypatch.setenv(k, v)
+        ctx = _ctx(m, v_e_max=64.0)
+        ctx.configure(v_e=48.0, seed=4, prefetch_rows_i=[256, 256])
+        ys, trs = [], []
+        for t in toks:
+            for i in range(2):
+                y = torch.empty(1, S.d, dtype=torch.float32, device="cuda")
+                tr = ctx.layer_forward(i, t[i].cuda(), y, flags=api.M.FUSE_PREDICT)
+                torch.cuda.synchronize()
+                ys.append(y.cpu().numpy())
+                trs.append((tr.act, tr.adm, tr.plan, tr.pcie_ondemand))
+        out.append((ys, trs))
+        ctx.close()
+    assert out[0][1] == out[1][1]
+    for a, b in zip(out[0][0], out[1][0]):
+        if "MOEPIC_COPY_STREAMS" in env:
+            np.testing.assert_array_equal(a, b)
+        else:
+            assert rel_err(b, a) <= 1e-5
+
+
+def test_profile_class_mask():
+    """moepic_profile(MOEPIC_PROFILE_CLASSES | 1 << class): only that class is event-timed."""
+    api = _api()
+    S = synth.SHAPES["qwen3"]
+    m = Model(2, S.N, S.K, S.d, S.I, L_host=1, seed=1, gen_device="cuda")
+    ctx = _ctx(m, v_e_max=64.0)
+    ctx.configure(v_e=32.0, seed=1)
+    H = synth.hidden_states(3, 4, 2, S.d)
+    ctx.profile(api.M.PROFILE_CLASSES | (1 << api.M.KERNEL_EXPERT))
+    for t in range(4):
+        for i in range(2):
+            y = torch.empty(1, S.d, dtype=torch.float32, device="cuda")
+            ctx.layer_forward(i, H[t, i][None].cuda(), y, flags=api.M.FUSE_PREDICT)
+    torch.cuda.synchronize()
+    k1, k2 = ctx.profile_read(api.M.KERNEL_ROUTER), ctx.profile_read(api.M.KERNEL_EXPERT)
+    assert k1["launches"] == 0 and k2["launches"] >= 8 and k2["kernel_ms"] > 0
+    ctx.profile(True)
+    for i in range(2):
+        y = torch.empty(1, S.d, dtype=torch.float32, device="cuda")
+        ctx.layer_forward(i, H[0, i][None].cuda(), y, flags=api.M.FUSE_PREDICT)
+    torch.cuda.synchronize()
+    assert ctx.profile_read(api.M.KERNEL_ROUTER)["launches"] == 2
+    ctx.close()
