@@ -1090,8 +1090,14 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       return fail(&ctx->err, MOEPIC_ERUNTIME, "workspace overflow (%lld floats)", (long long)ws_next);
     int tb = 1;
     while (tb < maxtok) tb <<= 1;
-    uint64_t alg_bytes = (uint64_t)R * ctx->rb();
-    for (size_t i = i0; i < i1; ++i) alg_bytes += (uint64_t)__builtin_popcount(work[i].mask) * d * 2;
+    // algorithmic bytes: each segment's rows once -- a segment split into token
+    // groups streams its rows once per group, but only the first group counts -- plus activations
+    uint64_t alg_bytes = 0;
+    for (size_t i = i0; i < i1; ++i) {
+      if (i == 0 || work[i].base != work[i - 1].base || work[i].nrows != work[i - 1].nrows)
+        alg_bytes += (uint64_t)work[i].nrows * ctx->rb();
+      alg_bytes += (uint64_t)__builtin_popcount(work[i].mask) * d * 2;
+    }
     // the last launch of the step's last group also combines (grid barrier, no K3 launch)
     kp.combine = 0;
     if (fuse && i1 == work.size() && comb.size() <= (size_t)kMaxLaunchSegs) {
