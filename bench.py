@@ -68,6 +68,11 @@ MODES = {
     "prefetch-only": dict(v_e=0.0, adaptive=False),                 # V_i = 0
     "lru-prefetch": dict(theta=1.0, policy="LRU", adaptive=False),  # ~ Mixtral-offloading / AdapMoE
     "lfu-prefetch": dict(theta=1.0, policy="LFU", adaptive=False),  # ~ MoE-Infinity
+    "no-sp": dict(random_prediction=True),                          # w/o SP: plans from a random h
+    "theta-0.25": dict(theta=0.25, adaptive=False),                 # theta sweep, uniform V_i
+    "theta-0.75": dict(theta=0.75, adaptive=False),
+    "zeta-0.002": dict(zeta=0.002),                                 # Alg. 1 granularity
+    "zeta-0.05": dict(zeta=0.05),
 }
 
 
@@ -293,11 +298,21 @@ def run_ours(args, log):
 
     # one decode token through the L layers; with a group (EP / TP) every rank passes the same h
     # and the library sums the partial outputs over the group inside layer_forward
+    # NEXT-1 "w/o SP": the next layer's plan comes from the predictor run on a random hidden state
+    # (moepic_predict_prefetch after each layer) instead of the fused predictor on h^i (Eq. 3)
+    hrand = None
+    if MODES[args.mode].get("random_prediction"):
+        hrand = synth.batch_hidden(4242, L * B, S.d).to("cuda").view(L, B, S.d)
+
     def token(t):
         for i in range(L):
             if attn:
                 attn(i)
-            ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=F, trace=False)
+            if hrand is None:
+                ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=F, trace=False)
+            else:
+                ctx.layer_forward(i, H[i, t * B:(t + 1) * B], y, stream=stream, flags=0, trace=False)
+                ctx.predict_prefetch((i + 1) % L, hrand[(i + t) % L], stream=stream, trace=False)
 
     # EP prefill: T/G tokens per rank, MOEPIC_TOKENS_SHARDED: the library
     # all-gathers the routing, dispatches each row to the ranks owning its experts, computes the
@@ -383,7 +398,8 @@ def run_ours(args, log):
     if adapt_tokens:
         t0 = time.time()
         solved = ctx.configure(use_solver=True, t_att=t_att, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
-                               zeta=0.01, **{k: v for k, v in base_cfg.items() if k != "theta_i"})
+                               zeta=MODES[args.mode].get("zeta", 0.01),
+                               **{k: v for k, v in base_cfg.items() if k != "theta_i"})
         alg1_in = {"inputs": args.alg1_inputs, "t_load_exp_ms": round(t_load, 6), "t_moe_ms": round(t_moe, 6),
                    "t_att_ms": round(t_att, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
         log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(solved['theta_eff_i']):.2f}.."
