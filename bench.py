@@ -66,6 +66,7 @@ MODES = {
     "no-lcp": dict(policy="RND"),                                   # random replacement
     "cache-only": dict(theta=1.0, prefetch=False, adaptive=False),  # theta = 1, no prefetch
     "prefetch-only": dict(v_e=0.0, adaptive=False),                 # V_i = 0
+    "lcp-prefetch": dict(theta=1.0, adaptive=False),                # LCP + SP at theta = 1 (no split)
     "lru-prefetch": dict(theta=1.0, policy="LRU", adaptive=False),  # ~ Mixtral-offloading / AdapMoE
     "lfu-prefetch": dict(theta=1.0, policy="LFU", adaptive=False),  # ~ MoE-Infinity
     "no-sp": dict(random_prediction=True),                          # w/o SP: plans from a random h
@@ -244,6 +245,7 @@ def run_ours(args, log):
     base_cfg = dict(v_e=v_e, theta_i=[cfg["theta"]] * L, y_cap_i=[y_cap] * L, seed=0)
     window_rows = None
     window_us = None
+    idle_us = None
     rbytes = 6 * S.d if args.weights == "bf16" else (3 * (S.d // 2) + 3 * (S.d // 64) * 4 + 15) // 16 * 16
     if args.prefetch_window_us not in ("auto", "0", "0.0"):   # reading Q30: a fixed window per layer
         window_us = float(args.prefetch_window_us)
@@ -259,8 +261,11 @@ def run_ours(args, log):
         base_cfg["v_e"] = mode["v_e"]
     if mode.get("adaptive") is False:
         cfg["adaptive"] = False
-    # reading Q30: the measured window applies to every decode mode that prefetches
+    # reading Q30: the measured window applies to every decode mode that prefetches.  The link-idle
+    # calibration tokens run in every decode run (window or not), so the timed tokens are the same
+    # tokens whatever the window setting
     auto_window = args.prefetch_window_us == "auto" and base_cfg.get("prefetch", 1) and not cfg.get("prefill")
+    calibrate = not cfg.get("prefill")
     ctx.configure(**base_cfg)
     log(f"[bench] configure (re-layout {v_e:.0f} tops) {time.time() - t0:.1f}s")
     transport = None
@@ -268,9 +273,13 @@ def run_ours(args, log):
         transport = args.transport
         ctx.join_process_group(api.M.TRANSPORT_NCCL if transport == "nccl" else api.M.TRANSPORT_PEER)
         log(f"[bench] rank {rank} joined the {parallel} group ({transport} transport)")
-    adapt_tokens = 2 * args.tau if cfg.get("adaptive") else 0
-    cal_tokens = 8 if auto_window else 0   # link-idle calibration before Alg. 1 (reading Q30)
-    pre_tokens = adapt_tokens + cal_tokens
+    # decode runs consume the same tokens in every mode: 2 tau warm tokens (the Alg. 1 adaptation
+    # period when the mode adapts, plain warm-up of the cache state otherwise), the link-idle
+    # calibration, the warm-up, then the timed tokens -- so the ablation rows time the same tokens
+    warm_tokens = 2 * args.tau if not cfg.get("prefill") else 0
+    adapt_tokens = warm_tokens if cfg.get("adaptive") else 0
+    cal_tokens = 8 if calibrate else 0   # link-idle calibration (reading Q30)
+    pre_tokens = warm_tokens + cal_tokens
     T = pre_tokens + args.warmup + args.steps
     # token t, layer i uses rows [t*B, (t+1)*B) of a [T*B][L][d] organic hidden-state process
     # stored [L][tokens][d] so every per-layer batch slice is a contiguous [B][d] block
@@ -346,6 +355,9 @@ def run_ours(args, log):
         log(f"[bench] attention stand-in {t_att * 1e3:.1f} us per layer (S = {args.attention})")
     solved = None
     alg1_in = None
+    if warm_tokens and not adapt_tokens:   # fixed-layout modes: the same warm tokens, no solver
+        for t in range(warm_tokens):
+            step(t)
     if adapt_tokens:
         # Alg. 1 outer loop: run 2 tau tokens on the uniform theta = 0.5 layout, profile
         # T_moe on this GPU and T_load^exp = U_e / PCIe, then reconfigure with the solver.
@@ -363,18 +375,33 @@ def run_ours(args, log):
         else:   # fixed, modelled profile (reproducible run to run): link and HBM rates
             t_load = U_e / (ALG1_PCIE_GBS * 1e9) * 1e3             # of this pool's boxes, K experts'
             t_moe = S.K * B * U_e / (ALG1_HBM_GBS * 1e9) * 1e3 + ALG1_LAUNCH_MS   # rows + launch cost
+    def solve(cfg_extra):
+        t0 = time.time()
+        res = ctx.configure(use_solver=True, t_att=t_att, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
+                            zeta=MODES[args.mode].get("zeta", 0.01),
+                            **{k: v for k, v in dict(base_cfg, **cfg_extra).items() if k != "theta_i"})
+        log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(res['theta_eff_i']):.2f}.."
+            f"{max(res['theta_eff_i']):.2f}, C {min(res['C_i'])}..{max(res['C_i'])}")
+        return res
+
+    if adapt_tokens:
+        snap = ctx.get_stats()   # Alg. 1's statistics after the adaptation tokens
+        solved = solve({})
+        alg1_in = {"inputs": args.alg1_inputs, "t_load_exp_ms": round(t_load, 6), "t_moe_ms": round(t_moe, 6),
+                   "t_att_ms": round(t_att, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
     if cal_tokens:
         # the prefetch window of this stack (P:389 / P:412 T_wind, reading Q30): with no attention
         # block the link idles per layer for the serial chain final K2 -> router -> host -> first
-        # copy (profiles/r02_decode_chain_timeline.md).  Measured as (layer time - PCIe bytes /
-        # link rate) over cal_tokens tokens (no timing events), rounded to 10 us so the
-        # configuration reproduces run to run; the plan of every layer is cut at that many rows of
-        # link time.  It is not fed back into Alg. 1 as T_att: re-solving with it moved DeepSeek to
-        # smaller theta and lost 3.5 % (Mixtral 0.9 %) against the cut alone (Q30).
+        # copy (profiles/r02_decode_chain_timeline.md).  Measured on the configured layout as
+        # (layer time - PCIe bytes / link rate) over cal_tokens tokens (no timing events), rounded
+        # to 10 us so the configuration reproduces run to run; the plan of every layer is then cut
+        # at that many rows of link time.  The configuration is solved again on the statistics
+        # of the adaptation tokens alone (snapshot restored), so the window is the only change;
+        # it is not fed to Alg. 1 as T_att (that moved DeepSeek to smaller theta, -3.5 %).
         cc0 = ctx.counters()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
-        for t in range(adapt_tokens, pre_tokens):
+        for t in range(warm_tokens, pre_tokens):
             step(t)
         a1.record(stream)
         torch.cuda.synchronize()
@@ -383,27 +410,21 @@ def run_ours(args, log):
         link_ms = (cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] - cc0["pcie_ondemand_bytes"]
                    - cc0["pcie_prefetch_bytes"]) / (cal_tokens * L) / (ALG1_PCIE_GBS * 1e9) * 1e3
         # three quarters of it: the next layer's on-demand copies queue behind the prefetch (one
-        # FIFO copy stream), so the window leaves their DMA start-up its own margin (measured:
-        # the full idle moved DeepSeek -3.3 %, three quarters +0.8 %; Qwen3 +3.4 % / +1.6 %)
-        window_us = max(0.0, round(0.75 * (lay_ms - link_ms) * 1e3 / 10.0) * 10.0)
-        if dist:   # one window for the whole group (rank 0's), so every rank plans alike
+        # FIFO copy stream), so the window leaves their DMA start-up its own margin
+        idle_us = (lay_ms - link_ms) * 1e3
+        window_us = max(0.0, round(0.75 * idle_us / 10.0) * 10.0) if auto_window else window_us
+        if dist and window_us is not None:   # one window for the whole group (rank 0's)
             wt = torch.tensor([window_us], device="cuda")
             dist.broadcast(wt, 0)
             window_us = float(wt.item())
-        window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
-        base_cfg["prefetch_rows_i"] = [window_rows] * L
-        log(f"[bench] link-idle window {window_us:.0f} us per layer ({window_rows} rows)")
-        if not adapt_tokens:   # fixed layouts (ablation modes): the same configuration, plus the window
-            ctx.configure(**base_cfg)
-    if adapt_tokens:
-        t0 = time.time()
-        solved = ctx.configure(use_solver=True, t_att=t_att, t_moe=t_moe, t_head=0.0, t_load_exp=t_load,
-                               zeta=MODES[args.mode].get("zeta", 0.01),
-                               **{k: v for k, v in base_cfg.items() if k != "theta_i"})
-        alg1_in = {"inputs": args.alg1_inputs, "t_load_exp_ms": round(t_load, 6), "t_moe_ms": round(t_moe, 6),
-                   "t_att_ms": round(t_att, 6), "t_head_ms": 0.0, "t_moe_measured_ms": round(t_moe_measured, 6)}
-        log(f"[bench] Alg. 1 reconfigure {time.time() - t0:.1f}s: theta {min(solved['theta_eff_i']):.2f}.."
-            f"{max(solved['theta_eff_i']):.2f}, C {min(solved['C_i'])}..{max(solved['C_i'])}")
+        if window_us is not None:
+            window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
+            base_cfg["prefetch_rows_i"] = [window_rows] * L
+        log(f"[bench] link idle {idle_us:.0f} us per layer; window {window_us} us ({window_rows} rows)")
+        ctx.configure(**base_cfg)   # back to the uniform allocation Alg. 1 started from (Q19) + the window
+        if adapt_tokens:
+            ctx.set_stats(snap)
+            solved = solve({})
     for t in range(pre_tokens, pre_tokens + args.warmup):
         step(t)
     torch.cuda.synchronize()
@@ -555,7 +576,8 @@ def run_ours(args, log):
                                                              theta_eff_i=[round(x, 4) for x in solved["theta_eff_i"]],
                                                              C_i=solved["C_i"]),
                    "y_cap": y_cap, "prefetch_window": None if window_rows is None else
-                   {"us": window_us, "rows": window_rows, "source": "measured link idle (auto)" if auto_window
+                   {"us": window_us, "rows": window_rows, "link_idle_us": round(idle_us, 1) if cal_tokens else None,
+                    "source": "measured link idle (auto)" if auto_window
                     else "--prefetch-window-us"},
                    "build_id": _build.build_id(),
                    "l2": "inputs larger than L2 (>=700 MB of expert rows streamed per layer)"},
