@@ -425,10 +425,23 @@ def run_ours(args, log):
             window_rows = int(window_us * 1e-6 * ALG1_PCIE_GBS * 1e9 // rbytes)
             base_cfg["prefetch_rows_i"] = [window_rows] * L
         log(f"[bench] link idle {idle_us:.0f} us per layer; window {window_us} us ({window_rows} rows)")
-        ctx.configure(**base_cfg)   # back to the uniform allocation Alg. 1 started from (Q19) + the window
+    # The state the timed tokens start from, re-created before the e2e tokens so that both arms
+    # consume the SAME tokens from the SAME cache state and statistics (the control plane is
+    # deterministic given both): back to the uniform allocation Alg. 1 started from (Q19) + the
+    # window, the adaptation statistics restored and Alg. 1 solved again; fixed-layout modes
+    # restore the statistics (LCP counters) before the re-layout, which ranks the cached set by them
+    s_pre = None if adapt_tokens else ctx.get_stats()
+
+    def reset_state():
         if adapt_tokens:
+            ctx.configure(**base_cfg)
             ctx.set_stats(snap)
-            solved = solve({})
+            return solve({})
+        ctx.set_stats(s_pre)
+        ctx.configure(**base_cfg)
+        return solved
+
+    solved = reset_state()
     for t in range(pre_tokens, pre_tokens + args.warmup):
         step(t)
     torch.cuda.synchronize()
@@ -480,12 +493,19 @@ def run_ours(args, log):
         # this rank's host rows of each e2e token: the whole batch (decode, replicated) or its T/G rows
         lo, hi = (rank * Bl, (rank + 1) * Bl) if sharded else (0, B)
         fl = SH if sharded else F
+        # the device arm's tokens from the device arm's starting state: the same warm-up tokens
+        # (untimed) and then the same timed tokens, host buffers in and out
+        t_first = pre_tokens + args.warmup
         Hh = [[synth.bf16_bits(H[i, t * B + lo:t * B + hi].cpu()) for i in range(L)]
-              for t in range(T, T + args.e2e_steps)]
-        tw = T + args.e2e_steps   # one untimed token through the host-buffer path (warm-up, like the device arm)
-        for i in range(L):
-            ctx.layer_forward_host(i, synth.bf16_bits(H[i, tw * B + lo:tw * B + hi].cpu()), stream=stream, flags=fl,
-                                   trace=False)
+              for t in range(t_first, t_first + args.e2e_steps)]
+        Hw = [[synth.bf16_bits(H[i, t * B + lo:t * B + hi].cpu()) for i in range(L)]
+              for t in range(pre_tokens, t_first)]
+        if dist:
+            dist.barrier()
+        reset_state()
+        for hw in Hw:
+            for i in range(L):
+                ctx.layer_forward_host(i, hw[i], stream=stream, flags=fl, trace=False)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if dist:
@@ -506,8 +526,8 @@ def run_ours(args, log):
         e2e = {"value": round(args.e2e_steps * B / (ems / 1e3), 4), "unit": "tokens/s",
                "h2d_bytes_per_step": L * Bh * S.d * 2, "d2h_bytes_per_step": L * Bh * S.d * 4,
                "api": "moepic_layer_forward_host" + (" (per rank, group data plane inside)" if dist else "")}
-        # the e2e tokens are later tokens of the same process: their own PCIe bytes and path
-        # fraction separate the API's per-layer round trip from a different byte mix
+        # the same tokens as the device arm: their PCIe bytes match up to the timing-dependent
+        # cancel-at-router drops (Q7); the path fraction isolates the API's per-layer round trip
         ce1 = ctx.counters()
         e2e_pcie = (ce1["pcie_ondemand_bytes"] - ce0["pcie_ondemand_bytes"] +
                     ce1["pcie_prefetch_bytes"] - ce0["pcie_prefetch_bytes"])

@@ -58,6 +58,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Copy-stream gate (K2's gated rows): the copy stream writes a 32-bit sequence number to device
+// memory after the step's last on-demand copy (cuStreamWriteValue32, ordered after the copy).
+__device__ __forceinline__ bool gate_poll(const unsigned int* g, unsigned int val) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g) : "memory");
+  return (int)(v - val) >= 0;
+}
+// blocking form; a flag that never arrives (a failed copy) must not hang the GPU: trap after ~10 s
+__device__ __forceinline__ void gate_wait(const unsigned int* g, unsigned int val) {
+  const unsigned long long t0 = gtimer();
+  while (!gate_poll(g, val)) {
+    __nanosleep(32);
+    if (gtimer() - t0 > 10000000000ull) __trap();
+  }
+}
 __device__ __forceinline__ void stamp_start(unsigned long long* ts) {
   if (ts && threadIdx.x == 0) atomicMin(ts, gtimer());
 }

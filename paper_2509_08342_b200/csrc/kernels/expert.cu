@@ -39,6 +39,8 @@ constexpr int kStagesV2 = 4;
 struct Tile {
   int s;          // segment index
   int64_t row;    // first launch row
+  int64_t lim;    // end of the CTA's row range in the current phase
+  int ph;         // 0: ungated rows, 1: gated rows (after the copy-stream flag)
 };
 
 }  // namespace
@@ -78,14 +80,20 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   float* red = reinterpret_cast<float*>(redbar + 2);   // [2][kConsumerWarps][NV]
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int64_t R = p.total_rows;
   const int64_t G = gridDim.x;
-  const int64_t r0 = k2_row_lo(blockIdx.x, R, G), r1 = k2_row_lo(blockIdx.x + 1, R, G);
+  // Two row phases: rows [0, RA) split over the first ga CTAs, then the gated rows [RA, R) (the
+  // tail of the step's last on-demand copy, still in flight at launch) over the first gb CTAs;
+  // every CTA streams its phase-0 rows, then its phase-1 rows once the copy stream's flag says
+  // they have landed.  Ungated launches: RA = R, gb = 0.
+  const int64_t RA = p.rows_a, RB = p.total_rows - p.rows_a;
+  const int64_t c = blockIdx.x;
+  const int64_t a0 = c < p.ga ? k2_row_lo(c, RA, p.ga) : 0, a1 = c < p.ga ? k2_row_lo(c + 1, RA, p.ga) : 0;
+  const int64_t b0 = c < p.gb ? RA + k2_row_lo(c, RB, p.gb) : RA, b1 = c < p.gb ? RA + k2_row_lo(c + 1, RB, p.gb) : RA;
   stamp_start(p.tstamp);
   asm volatile("griddepcontrol.launch_dependents;");   // a PDL-launched router may get ready now
   unsigned long long* dbg = p.dbg ? p.dbg + (size_t)blockIdx.x * 8 : nullptr;   // phase trace (tools)
   if (dbg && tid == 0) dbg[0] = gtimer();
-  if (r0 >= r1) return;
+  if (a0 >= a1 && b0 >= b1 && !p.combine) return;   // (a combining launch: every CTA reaches the barrier)
 
   if (tid == 0) {
     for (int i = 0; i < kStagesV2; ++i) {
@@ -99,21 +107,32 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   __syncthreads();
 
   auto seg_end = [&](int s) -> int64_t { return (int64_t)p.segs[s].row_begin + p.segs[s].nrows; };
+  auto seek = [&](Tile& it) {   // first segment holding it.row (segments are in row order)
+    while (it.row < it.lim && seg_end(it.s) <= it.row) ++it.s;
+  };
   Tile start;
   start.s = 0;
-  while (seg_end(start.s) <= r0) ++start.s;
-  start.row = r0;
+  if (a0 < a1) {
+    start.row = a0, start.lim = a1, start.ph = 0;
+  } else {
+    start.row = b0, start.lim = b1, start.ph = 1;
+  }
+  seek(start);
   auto tile_end = [&](const Tile& it) -> int64_t {
     int64_t e = it.row + RS;
     const int64_t se = seg_end(it.s);
     if (e > se) e = se;
-    if (e > r1) e = r1;
+    if (e > it.lim) e = it.lim;
     return e;
   };
   auto advance = [&](Tile& it) {
     const int64_t e = tile_end(it);
     it.row = e;
     if (e >= seg_end(it.s)) ++it.s;
+    if (it.row >= it.lim && it.ph == 0) {   // phase 0 done: on to the gated rows
+      it.row = b0, it.lim = b1, it.ph = 1;
+      seek(it);
+    }
   };
 
   // ------------------------------------------------------------------ TMA producer (warp 0 lane 0)
@@ -123,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   uint64_t pol = 0;
   Tile pit = start;
   int pn = 0;   // next tile index to issue
+  bool gate_open = p.gate == nullptr;
   auto issue = [&]() {
     const int pst = pn % kStagesV2;
     const int64_t e = tile_end(pit);
@@ -133,9 +153,24 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     advance(pit);
     ++pn;
   };
+  // issue tiles pn..upto as far as the ring allows; a gated tile waits for the copy-stream flag
+  // only when `block` (the consumers need that very tile), else it is deferred, so the phase-0
+  // tiles already in the ring are consumed while the gated rows are still in flight
+  auto issue_upto = [&](int upto, bool block) {
+    while (pn <= upto && pit.row < pit.lim) {
+      if (pit.ph == 1 && !gate_open) {
+        if (block) gate_wait(p.gate, p.gate_val);
+        else if (!gate_poll(p.gate, p.gate_val)) return;
+        gate_open = true;
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // flag (generic) before the TMA reads
+      }
+      if (pn >= kStagesV2) mbar_wait(&empty[pn % kStagesV2], (pn / kStagesV2 - 1) & 1);
+      issue();
+    }
+  };
   if (producer) {
     pol = evict_first_policy();
-    while (pn < kStagesV2 && pit.row < r1) issue();
+    issue_upto(kStagesV2 - 1, false);
   }
 
   // ------------------------------------------------------------------ consumer warps
@@ -249,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   }
 
   Tile it = start;
-  for (int n = 0; it.row < r1; ++n) {
+  for (int n = 0; it.row < it.lim; ++n) {
     const int st = n % kStagesV2;
     const int s = it.s;
     const int nr = (int)(tile_end(it) - it.row);
@@ -288,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
         }
       }
     }
+    if (producer) issue_upto(n, true);   // (a no-op unless tile n was deferred at the gate)
     mbar_wait(&full[st], (n / kStagesV2) & 1);
     if (dbg && n == 0 && tid == 0) dbg[1] = gtimer();
     const uint8_t* tile = stages + (size_t)st * tileb;
@@ -374,10 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       phase2();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[prev_stage]);
-      if (producer && pit.row < r1) {   // refill tile n-1's stage with tile n-1+S
-        mbar_wait(&empty[prev_stage], ((n - 1) / kStagesV2) & 1);
-        issue();
-      }
+      if (producer) issue_upto(n - 1 + kStagesV2, false);   // refill tile n-1's stage with tile n-1+S
       if (prev_seg != s) flush(prev_seg, prev_ntok);
     }
 
@@ -473,6 +506,10 @@ struct K2ParamsCap {
   const float* w;
   float* ws;
   int64_t total_rows;
+  int64_t rows_a;
+  int ga, gb;
+  const unsigned int* gate;
+  unsigned int gate_val;
   int d, K, nsegs;
   Seg segs[CAP];
   int combine, B, residual, ncomb, flat;
@@ -488,6 +525,7 @@ template <int TB, int CW, int RS, int Q4, int CAP>
 static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   K2ParamsCap<CAP> q;
   q.h = p.h; q.ids = p.ids; q.w = p.w; q.ws = p.ws; q.total_rows = p.total_rows;
+  q.rows_a = p.rows_a; q.ga = p.ga; q.gb = p.gb; q.gate = p.gate; q.gate_val = p.gate_val;
   q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0; q.flat = p.flat;

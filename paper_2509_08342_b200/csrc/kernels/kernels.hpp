@@ -78,6 +78,14 @@ struct K2Params {
   const float* w;         // [B][K]
   float* ws;              // partial sums
   int64_t total_rows;
+  // gated rows: launch rows [rows_a, total_rows) are the tail of the step's last on-demand copy,
+  // still in flight at launch; CTAs stream them after *gate reaches gate_val (written by the copy
+  // stream after that copy).  rows [0, rows_a) over the first ga CTAs, the rest over the first gb.
+  // Ungated: rows_a = total_rows, ga = grid, gb = 0, gate = nullptr.
+  int64_t rows_a;
+  int ga, gb;
+  const unsigned int* gate;
+  unsigned int gate_val;
   int d, K, nsegs;
   int q4;                 // rows are Q4G64 (dequantised on the fly) instead of bf16
   Seg segs[kMaxLaunchSegs];

@@ -403,6 +403,20 @@ struct moepic_ctx {
   // decode: a step whose last on-demand copy is too small to split makes that whole copy the tail
   // (MOEPIC_OD_SPLIT_BOUNDARY=0 turns this off)
   bool od_split_boundary = true;
+  // decode, gated tail (MOEPIC_K2_GATE, default on): ONE K2 launch per step covers the resident,
+  // prefetched and on-demand rows; the tail of the last on-demand copy is still in flight at
+  // launch and the CTAs stream it after the copy stream's flag (cuStreamWriteValue32 after that
+  // copy).  The tail is sized so that it lands while K2 streams the rest (od_tail_auto: a
+  // fraction k2_gate_frac of the K2 time of the step's rows, at the measured link rate), so the
+  // gate rarely stalls, and the link idles only for the tail's few rows + the combine.  Without
+  // the gate (or when the step does not fit one K2 launch) the tail gets its own launch.
+  bool k2_gate = true;
+  bool od_tail_auto = true;
+  double k2_gate_frac = 0.8;
+  int64_t tail_split_x = 4;   // MOEPIC_TAIL_SPLIT_X
+  unsigned int gate_seq = 0;
+  using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  WriteValue32Fn write_value32 = nullptr;
   // MOEPIC_TIMELINE=<path> (tools): per decode layer step, %globaltimer stamps of the router, the
   // K2 launches before the final one, the final (combining) K2 and the completion of the step's
   // last on-demand copy (a one-thread kernel on the copy stream), plus host stamps of the call,
@@ -676,8 +690,20 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
       cudaMemset(ctx->arena + lay.rsel, 0, (size_t)desc->N * 16) != cudaSuccess)
     return bail(MOEPIC_ERUNTIME);
   if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;
-  if (const char* e = getenv("MOEPIC_OD_TAIL_MB")) ctx->od_tail_bytes = (size_t)atol(e) << 20;
-  if (const char* e = getenv("MOEPIC_OD_TAIL_KB")) ctx->od_tail_bytes = (size_t)atol(e) << 10;   // tests: small shapes
+  if (const char* e = getenv("MOEPIC_OD_TAIL_MB")) ctx->od_tail_bytes = (size_t)atol(e) << 20, ctx->od_tail_auto = false;
+  if (const char* e = getenv("MOEPIC_OD_TAIL_KB")) ctx->od_tail_bytes = (size_t)atol(e) << 10, ctx->od_tail_auto = false;   // tests: small shapes
+  if (const char* e = getenv("MOEPIC_K2_GATE")) ctx->k2_gate = atoi(e) != 0;
+  if (const char* e = getenv("MOEPIC_K2_GATE_FRAC")) ctx->k2_gate_frac = atof(e);
+  if (const char* e = getenv("MOEPIC_TAIL_SPLIT_X")) ctx->tail_split_x = std::max(2L, atol(e));
+  if (ctx->k2_gate) {   // the copy stream's flag write (driver API, resolved through the runtime)
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      ctx->write_value32 = reinterpret_cast<moepic_ctx::WriteValue32Fn>(fn);
+    else
+      ctx->k2_gate = false;
+  }
   if (const char* e = getenv("MOEPIC_OD_SPLIT_BOUNDARY")) ctx->od_split_boundary = atoi(e) != 0;
   if (const char* e = getenv("MOEPIC_PDL")) ctx->pdl = atoi(e) != 0;
   if (const char* e = getenv("MOEPIC_TIMELINE")) {
@@ -1010,12 +1036,33 @@ static moepic_status launch_group_tc(moepic_ctx* ctx, const std::vector<StepSeg>
   return MOEPIC_OK;
 }
 
+// Gated launch (K2Gate): segs[0, n_a) are ready at launch, segs[n_a, ...) are the tail of the
+// step's last on-demand copy, streamed by the same launch once the copy stream's flag arrives.
+constexpr size_t kGateOff = 32;   // the copy-stream gate word inside the arena's ticket block
+constexpr double kGateLaunchS = 3e-6;   // K2 ramp (the launch latency is left out: a tail that
+                                         // outlasts K2 stalls the gate, measured)
+
+struct K2Gate {
+  size_t n_a;
+  const unsigned int* flag;
+  unsigned int val;
+};
+
+// Can one gated K2 launch (with the fused combine) cover these segments?  Needs the CUDA-core K2
+// (every expert within K2's token block, so no K2T) and one parameter block.
+static bool k2_gate_feasible(const moepic_ctx* ctx, size_t nsegs, int B) {
+  const int tbmax = k2_max_tokens(ctx->desc.d, ctx->desc.weight_format == MOEPIC_Q4G64);
+  return ctx->k2_gate && B <= tbmax && nsegs <= (size_t)kMaxLaunchSegs;
+}
+
 static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& segs, const uint16_t* h, int B,
                                   cudaStream_t s, int64_t& ws_next, std::vector<CombineSeg>& comb, int& launches,
-                                  FuseCombine* fuse = nullptr) {
+                                  FuseCombine* fuse = nullptr, const K2Gate* gate = nullptr) {
   const int d = ctx->desc.d;
   const int tbmax = k2_max_tokens(d, ctx->desc.weight_format == MOEPIC_Q4G64);
-  if (ctx->k2t && B <= kK2TMaxB) {   // an expert with more tokens than K2's block: K2T reads it once
+  if (gate && (B > tbmax || !fuse))
+    return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: gated K2 launch outside K2's token block");
+  if (!gate && ctx->k2t && B <= kK2TMaxB) {   // an expert with more tokens than K2's block: K2T reads it once
     bool hot = false, ok = true;
     const uint8_t* rbase = ctx->arena + ctx->lay.shared;
     for (const auto& sg : segs) {
@@ -1027,7 +1074,10 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
   }
   // split by token groups of <= tbmax tokens
   std::vector<StepSeg> work;
-  for (const auto& sg : segs) {
+  size_t work_a = 0;   // gated: work items [0, work_a) are phase 0
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const auto& sg = segs[si];
+    if (gate && si == gate->n_a) work_a = work.size();
     if (sg.nrows <= 0 || sg.mask == 0) continue;
     uint32_t m = sg.mask;
     while (m) {
@@ -1042,17 +1092,30 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       work.push_back(x);
     }
   }
+  if (gate && gate->n_a >= segs.size()) work_a = work.size();
+  if (gate && (work.size() > (size_t)kMaxLaunchSegs || comb.size() + work.size() > (size_t)kMaxLaunchSegs))
+    return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: gated K2 launch over more than one parameter block");
   size_t i0 = 0;
   K2Params& kp = *ctx->kp;
   while (i0 < work.size()) {
     const size_t i1 = std::min(work.size(), i0 + (size_t)kMaxLaunchSegs);
-    int64_t R = 0;
+    int64_t R = 0, RA = 0;
     int maxtok = 1;
     for (size_t i = i0; i < i1; ++i) {
       R += work[i].nrows;
+      if (!gate || i < work_a) RA += work[i].nrows;
       maxtok = std::max(maxtok, __builtin_popcount(work[i].mask));
     }
-    const int64_t G = std::min<int64_t>(kSMs, R);
+    const int64_t RB = R - RA;
+    // phase 0 rows over the first GA CTAs, gated rows over the first GB (no CTA range is empty
+    // inside a phase, so every CTA between a segment's first and last owner writes a partial)
+    const int64_t G = std::min<int64_t>(kSMs, std::max(RA, RB));
+    const int64_t GA = std::min(G, RA), GB = std::min(G, RB);
+    kp.rows_a = RA;
+    kp.ga = (int)GA;
+    kp.gb = (int)GB;
+    kp.gate = gate ? gate->flag : nullptr;
+    kp.gate_val = gate ? gate->val : 0u;
     kp.h = h;
     kp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids);
     kp.w = reinterpret_cast<const float*>(ctx->arena + ctx->lay.w);
@@ -1070,14 +1133,17 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
       g.nrows = work[i].nrows;
       g.tok_mask = work[i].mask;
       g.row_begin = (int32_t)rb;
-      // CTA owning the first / last row: largest c with c*R/G <= row
-      const int64_t first = rb, last = rb + work[i].nrows - 1;
-      int64_t cf = (first * G) / R;
-      while (cf + 1 < G && k2_row_lo(cf + 1, R, G) <= first) ++cf;
-      while (k2_row_lo(cf, R, G) > first) --cf;
-      int64_t cl = (last * G) / R;
-      while (cl + 1 < G && k2_row_lo(cl + 1, R, G) <= last) ++cl;
-      while (k2_row_lo(cl, R, G) > last) --cl;
+      // CTA owning the first / last row of the segment within its phase: largest c with
+      // c*Rp/Gp <= row
+      const bool ph1 = rb >= RA;
+      const int64_t Rp = ph1 ? RB : RA, Gp = ph1 ? GB : GA, off = ph1 ? RA : 0;
+      const int64_t first = rb - off, last = rb - off + work[i].nrows - 1;
+      int64_t cf = (first * Gp) / Rp;
+      while (cf + 1 < Gp && k2_row_lo(cf + 1, Rp, Gp) <= first) ++cf;
+      while (k2_row_lo(cf, Rp, Gp) > first) --cf;
+      int64_t cl = (last * Gp) / Rp;
+      while (cl + 1 < Gp && k2_row_lo(cl + 1, Rp, Gp) <= last) ++cl;
+      while (k2_row_lo(cl, Rp, Gp) > last) --cl;
       g.cta_first = (int32_t)cf;
       const int ntok = __builtin_popcount(work[i].mask);
       const int nchunks = (int)(cl - cf + 1);
@@ -1634,8 +1700,25 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     if (c == kBeta || (c == kGamma && l.I_top < d.I)) ++n_copies;
     if (c == kGamma && l.I_top > 0) ++n_copies;
   }
+  // gated tail (one K2 launch per step, the last copy's tail streamed after the copy-stream flag)
+  const bool q4 = d.weight_format == MOEPIC_Q4G64;
+  const bool gate_mode = ctx->k2_gate && B <= k2_max_tokens(d.d, q4);
   const bool split_ok = B <= kDecodeMaxB && ctx->od_tail_bytes > 0;
-  const int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
+  int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
+  if (split_ok && gate_mode && ctx->od_tail_auto) {
+    // the tail lands while K2 streams the step's other rows: the link stays busy under K2 and the
+    // gated rows are streamed as they land.  Tail = k2_gate_frac x (K2 time of the step's rows +
+    // ~3 us ramp) at the link rate (K2 ~6 TB/s on bf16 rows, ~1.6 TB/s dequantising
+    // Q4G64; link ~55 GB/s, both measured); below 1 so that the gate itself rarely waits
+    int64_t step_rows = (int64_t)res.A.size() * d.I;
+    step_rows += (int64_t)d.n_shared * (shared_hi(cp) - shared_lo(cp));
+    const double k2_s = (double)step_rows * rb / (q4 ? 1.6e12 : 6.0e12) + kGateLaunchS;
+    tail_rows_split = std::max<int64_t>(1, (int64_t)(ctx->k2_gate_frac * k2_s * 55e9 / rb));
+  }
+  // a copy is split only when it is well above the tail (split_x x tail): every extra DMA costs
+  // ~4 us of link time (scripts/dma_probe.cu), a somewhat long whole-copy tail only a short wait
+  // at the gate
+  const int64_t split_min_rows = (gate_mode && ctx->od_tail_auto ? ctx->tail_split_x : 2) * tail_rows_split;
   const uint8_t* split_dst = nullptr;   // segment whose tail was split off
   bool split_whole = false;             // ... or which is the tail as a whole (ev_od_head before it)
   // Two copy streams (MOEPIC_COPY_STREAMS=2; default 1): the step's on-demand copies alternate
@@ -1676,7 +1759,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     if (cs != ctx->copy) {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs));
       ctx->ctr.h2d_copies++;
-    } else if (split_ok && last && (int64_t)rows > 2 * tail_rows_split) {
+    } else if (split_ok && last && (int64_t)rows > split_min_rows) {
       moepic_status st2 = join2();
       if (st2 != MOEPIC_OK) return st2;
       const size_t head = bytes - (size_t)tail_rows_split * rb;
@@ -1685,7 +1768,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
       CK(cudaMemcpyAsync(dst + head, src + head, bytes - head, cudaMemcpyHostToDevice, ctx->copy));
       ctx->ctr.h2d_copies += 2;
       split_dst = dst;
-    } else if (split_ok && ctx->od_split_boundary && last && n_copies >= 2) {
+    } else if (split_ok && ctx->od_split_boundary && last && (n_copies >= 2 || gate_mode)) {
       // a small last copy is the tail as a whole: the K2 launch over everything else waits for
       // the copies before it, so only the last copy's rows remain after the link goes quiet
       moepic_status st2 = join2();
@@ -1715,6 +1798,24 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   }
   std::vector<uint32_t> masks(res.A.size());
   std::vector<uint8_t*> od_rest(d.N, nullptr);   // gamma with a prefetched prefix: where row `prefix` lands
+  // gated tail: the step's last copy should be a small one -- a bottom rather than a gamma top
+  // (I_top rows) -- so that it can be the tail whole, without an extra DMA.  With gamma tops to
+  // copy in pass 2, the last pass-1 bottom is held back and issued after them (the link is busy
+  // with the copies before it meanwhile).
+  int defer_a = -1;
+  if (gate_mode && split_ok && ctx->od_tail_auto && l.I_top > 0) {
+    bool pass2 = false;
+    for (size_t a = 0; a < res.A.size(); ++a)
+      if (res.cls[a] == kGamma && res.plan_idx[a] < 0) pass2 = true;
+    int n1 = 0;   // pass-1 bottoms: hold one back only if another keeps the link busy meanwhile
+    if (pass2)
+      for (size_t a = 0; a < res.A.size(); ++a)
+        if (res.plan_idx[a] < 0 && (res.cls[a] == kBeta || (res.cls[a] == kGamma && l.I_top < d.I))) {
+          defer_a = (int)a;
+          ++n1;
+        }
+    if (n1 < 2) defer_a = -1;
+  }
   for (size_t a = 0; a < res.A.size(); ++a) {   // pass 1: everything classification decides
     const int e = res.A[a];
     const uint32_t m = masks[a] = mask_of(e);
@@ -1734,7 +1835,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
         gC.push_back(StepSeg{dst, e, rows, m, r0});
         od_row += rows;
       }
-    } else if (c == kBeta || (c == kGamma && l.I_top < d.I)) {
+    } else if ((c == kBeta || (c == kGamma && l.I_top < d.I)) && (int)a != defer_a) {
       // missing bottom rows [I_top, I): known from classification alone (a gamma expert's top
       // rows follow in pass 2, once admission has chosen their destination)
       const int rows = d.I - l.I_top;
@@ -1773,6 +1874,15 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     if ((st = copy(top, ctx->host_expert(layer, e), l.I_top, slot >= 0)) != MOEPIC_OK) return st;
     gC.push_back(StepSeg{top, e, l.I_top, masks[a], 0});
   }
+  if (defer_a >= 0) {   // the held-back bottom: the step's last copy
+    const int e = res.A[defer_a];
+    const int rows = d.I - l.I_top;
+    uint8_t* dst = ctx->od_ptr(buf, od_row);
+    if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
+    if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)l.I_top * rb, rows)) != MOEPIC_OK) return st;
+    gC.push_back(StepSeg{dst, e, rows, masks[defer_a], l.I_top});
+    od_row += rows;
+  }
   // the split copy's segment is the last one pushed to gC: cut its tail into its own segment
   const uint8_t* tail_base = nullptr;
   if (split_dst) {
@@ -1794,6 +1904,15 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   if ((st = join2()) != MOEPIC_OK) return st;
   if (n_od && ctx->tl_slot(2)) launch_stamp(ctx->tl_slot(2), ctx->copy);
   if (n_od) CK(cudaEventRecord(ctx->ev_od, ctx->copy));
+  bool gated = false;          // the flag follows this step's last on-demand copy
+  bool gate_consumed = false;  // ... and the single K2 launch streams the tail behind it
+  if (tail_base && gate_mode && ctx->write_value32) {
+    const CUdeviceptr flag = (CUdeviceptr)(ctx->arena + ctx->lay.ticket + kGateOff);
+    if (ctx->write_value32((CUstream)ctx->copy, flag, (cuuint32_t)(ctx->gate_seq + 1), 0) != CUDA_SUCCESS)
+      return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "cuStreamWriteValue32 failed");
+    ++ctx->gate_seq;
+    gated = true;
+  }
   {   // an expert's on-demand segments consecutive, tops first (the prefill down GEMM groups by expert)
     std::vector<int32_t> pos(d.N, 0);
     for (size_t a = 0; a < res.A.size(); ++a) pos[res.A[a]] = (int32_t)a;
@@ -1825,11 +1944,22 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     std::vector<StepSeg> tail(gC.end() - 1, gC.end());
     if (!gB.empty()) CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
     CK(cudaStreamWaitEvent(s, ctx->ev_od_head, 0));
-    st = launch_group(ctx, first, h, B, s, ws_next, comb, launches, nullptr);
-    if (st != MOEPIC_OK) return st;
-    CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
-    st = launch_group(ctx, tail, h, B, s, ws_next, comb, launches, &fuse);
-    if (st != MOEPIC_OK) return st;
+    if (gated && tail[0].mask != 0 && k2_gate_feasible(ctx, first.size() + 1, B)) {
+      // ONE launch: everything but the tail now, the tail behind the copy-stream flag
+      const K2Gate gate{first.size(), reinterpret_cast<const unsigned int*>(ctx->arena + ctx->lay.ticket + kGateOff),
+                        ctx->gate_seq};
+      std::vector<StepSeg> all(first);
+      all.push_back(tail[0]);
+      st = launch_group(ctx, all, h, B, s, ws_next, comb, launches, &fuse, &gate);
+      if (st != MOEPIC_OK) return ctx->poisoned = true, st;
+      gate_consumed = true;
+    } else {
+      st = launch_group(ctx, first, h, B, s, ws_next, comb, launches, nullptr);
+      if (st != MOEPIC_OK) return st;
+      CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
+      st = launch_group(ctx, tail, h, B, s, ws_next, comb, launches, &fuse);
+      if (st != MOEPIC_OK) return st;
+    }
   } else {
   const bool lastA = gB.empty() && gC.empty(), lastB = gC.empty();
   st = launch_group(ctx, gA, h, B, s, ws_next, comb, launches, lastA ? &fuse : nullptr);
@@ -1869,7 +1999,9 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   }
   }
   // admitted experts that arrived as full prefetches (or a prefix of one, Q30): D2D their top
-  // rows -- from the plan buffer, and past the prefix from the on-demand region
+  // rows -- from the plan buffer, and past the prefix from the on-demand region (after a gated
+  // launch the compute stream has not waited for the copy event itself: it does here)
+  bool od_synced = !gate_consumed;
   for (const auto& a : res.adm) {
     if (!a.d2d_from_plan || a.victim == kAdmNone || l.I_top == 0) continue;
     const int pj = [&] { for (size_t k = 0; k < used.items.size(); ++k) if (used.items[k].expert == a.expert) return (int)k; return -1; }();
@@ -1879,6 +2011,8 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
                        (size_t)pre * rb, cudaMemcpyDeviceToDevice, s));
     if (pre < l.I_top) {
       if (!od_rest[a.expert]) return fail(&ctx->err, MOEPIC_ERUNTIME, "internal: prefix rest not on demand");
+      if (!od_synced) CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
+      od_synced = true;
       CK(cudaMemcpyAsync(ctx->slot_ptr(layer, a.slot) + (size_t)pre * rb, od_rest[a.expert],
                          (size_t)(l.I_top - pre) * rb, cudaMemcpyDeviceToDevice, s));
     }
