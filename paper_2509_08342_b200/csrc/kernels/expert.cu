@@ -39,8 +39,6 @@ constexpr int kStagesV2 = 4;
 struct Tile {
   int s;          // segment index
   int64_t row;    // first launch row
-  int64_t lim;    // end of the CTA's row range in the current phase
-  int ph;         // 0: ungated rows, 1: gated rows (after the copy-stream flag)
 };
 
 }  // namespace
@@ -107,70 +105,72 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   __syncthreads();
 
   auto seg_end = [&](int s) -> int64_t { return (int64_t)p.segs[s].row_begin + p.segs[s].nrows; };
-  auto seek = [&](Tile& it) {   // first segment holding it.row (segments are in row order)
-    while (it.row < it.lim && seg_end(it.s) <= it.row) ++it.s;
+  auto seg_of = [&](int64_t row, int64_t lim) {   // first segment holding row (segments in row order)
+    int s = 0;
+    while (row < lim && seg_end(s) <= row) ++s;
+    return s;
   };
-  Tile start;
-  start.s = 0;
-  if (a0 < a1) {
-    start.row = a0, start.lim = a1, start.ph = 0;
-  } else {
-    start.row = b0, start.lim = b1, start.ph = 1;
-  }
-  seek(start);
-  auto tile_end = [&](const Tile& it) -> int64_t {
+  const int sA = seg_of(a0, a1), sB = seg_of(b0, b1);
+  auto tile_end = [&](const Tile& it, int64_t lim) -> int64_t {
     int64_t e = it.row + RS;
     const int64_t se = seg_end(it.s);
     if (e > se) e = se;
-    if (e > it.lim) e = it.lim;
+    if (e > lim) e = lim;
     return e;
   };
-  auto advance = [&](Tile& it) {
-    const int64_t e = tile_end(it);
+  auto advance = [&](Tile& it, int64_t lim) {
+    const int64_t e = tile_end(it, lim);
     it.row = e;
     if (e >= seg_end(it.s)) ++it.s;
-    if (it.row >= it.lim && it.ph == 0) {   // phase 0 done: on to the gated rows
-      it.row = b0, it.lim = b1, it.ph = 1;
-      seek(it);
-    }
   };
 
   // ------------------------------------------------------------------ TMA producer (warp 0 lane 0)
   // Prologue fills every stage; afterwards tile n-1+S is issued into tile n-1's stage as soon as
-  // all warps released it (in iteration n, right after warp 0's own release).
+  // all warps released it (in iteration n, right after warp 0's own release).  The producer walks
+  // the CTA's phase-0 rows, then its gated rows.
   const bool producer = tid == 0;
   uint64_t pol = 0;
-  Tile pit = start;
+  Tile pit;
+  int64_t plim;
+  bool pgated;
+  if (a0 < a1) pit.s = sA, pit.row = a0, plim = a1, pgated = false;
+  else pit.s = sB, pit.row = b0, plim = b1, pgated = true;
   int pn = 0;   // next tile index to issue
-  bool gate_open = p.gate == nullptr;
+  // wait for the copy-stream flag; the CTA's wait (ns) feeds the host's tail-size controller
+  auto gate_pass = [&]() {
+    const unsigned long long t0 = gtimer();
+    gate_wait(p.gate, p.gate_val);
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // flag (generic) before the TMA reads
+    if (p.stall) {
+      const unsigned long long w = gtimer() - t0;
+      p.stall[blockIdx.x] = w > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned int)w;
+    }
+  };
   auto issue = [&]() {
     const int pst = pn % kStagesV2;
-    const int64_t e = tile_end(pit);
+    const int64_t e = tile_end(pit, plim);
     const Seg& sg = p.segs[pit.s];
     const uint32_t bytes = (uint32_t)((e - pit.row) * rowb);
     mbar_expect_tx(&full[pst], bytes);
     bulk_g2s(stages + (size_t)pst * tileb, sg.base + (pit.row - sg.row_begin) * rowb, bytes, &full[pst], pol);
-    advance(pit);
+    advance(pit, plim);
     ++pn;
   };
-  // issue tiles pn..upto as far as the ring allows; a gated tile waits for the copy-stream flag
-  // only when `block` (the consumers need that very tile), else it is deferred, so the phase-0
-  // tiles already in the ring are consumed while the gated rows are still in flight
-  auto issue_upto = [&](int upto, bool block) {
-    while (pn <= upto && pit.row < pit.lim) {
-      if (pit.ph == 1 && !gate_open) {
-        if (block) gate_wait(p.gate, p.gate_val);
-        else if (!gate_poll(p.gate, p.gate_val)) return;
-        gate_open = true;
-        asm volatile("fence.proxy.async.global;" ::: "memory");   // flag (generic) before the TMA reads
-      }
-      if (pn >= kStagesV2) mbar_wait(&empty[pn % kStagesV2], (pn / kStagesV2 - 1) & 1);
-      issue();
-    }
+  // is there a tile to issue?  Once the phase-0 rows are issued, switch to the gated rows and wait
+  // (once) for the copy-stream flag: warp 0 waits with it, the tiles already in the ring complete
+  // on their own and are consumed once the flag is seen
+  auto more = [&]() -> bool {
+    if (pit.row < plim) return true;
+    if (pgated) return false;
+    pit.s = sB, pit.row = b0, plim = b1, pgated = true;
+    if (pit.row >= plim) return false;
+    if (p.gate) gate_pass();
+    return true;
   };
   if (producer) {
     pol = evict_first_policy();
-    issue_upto(kStagesV2 - 1, false);
+    if (pgated && p.gate) gate_pass();   // a CTA with gated rows only
+    while (pn < kStagesV2 && more()) issue();
   }
 
   // ------------------------------------------------------------------ consumer warps
@@ -283,11 +283,17 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     for (int c = 0; c < CW; ++c) yacc[t][c] = 0.f;
   }
 
-  Tile it = start;
-  for (int n = 0; it.row < it.lim; ++n) {
+  int n = 0;
+  // the CTA's phase-0 rows, then its gated rows: the same loop body instantiated for each range
+  // (a loop-invariant range end keeps the tile walk in the uniform datapath, as with one range)
+  auto run_range = [&](const int64_t r0, const int64_t r1, const int s0) {
+  Tile it;
+  it.s = s0;
+  it.row = r0;
+  for (; it.row < r1; ++n) {
     const int st = n % kStagesV2;
     const int s = it.s;
-    const int nr = (int)(tile_end(it) - it.row);
+    const int nr = (int)(tile_end(it, r1) - it.row);
     if (s != cur) {                      // new segment: its tokens, weights and h columns
       cur = s;
       const Seg& sg = p.segs[s];
@@ -323,7 +329,6 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
         }
       }
     }
-    if (producer) issue_upto(n, true);   // (a no-op unless tile n was deferred at the gate)
     mbar_wait(&full[st], (n / kStagesV2) & 1);
     if (dbg && n == 0 && tid == 0) dbg[1] = gtimer();
     const uint8_t* tile = stages + (size_t)st * tileb;
@@ -410,7 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       phase2();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[prev_stage]);
-      if (producer) issue_upto(n - 1 + kStagesV2, false);   // refill tile n-1's stage with tile n-1+S
+      if (producer && more()) {   // refill tile n-1's stage with tile n-1+S
+        mbar_wait(&empty[prev_stage], ((n - 1) / kStagesV2) & 1);
+        issue();
+      }
       if (prev_seg != s) flush(prev_seg, prev_ntok);
     }
 
@@ -447,8 +455,11 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     prev_nr = nr;
     prev_seg = s;
     prev_ntok = ntok;
-    advance(it);
+    advance(it, r1);
   }
+  };
+  run_range(a0, a1, sA);
+  run_range(b0, b1, sB);
   if (prev_stage >= 0) {
     phase2();
     flush(prev_seg, prev_ntok);
@@ -510,6 +521,7 @@ struct K2ParamsCap {
   int ga, gb;
   const unsigned int* gate;
   unsigned int gate_val;
+  unsigned int* stall;
   int d, K, nsegs;
   Seg segs[CAP];
   int combine, B, residual, ncomb, flat;
@@ -525,7 +537,7 @@ template <int TB, int CW, int RS, int Q4, int CAP>
 static void k2_launch_t(const K2Params& p, int grid, cudaStream_t s) {
   K2ParamsCap<CAP> q;
   q.h = p.h; q.ids = p.ids; q.w = p.w; q.ws = p.ws; q.total_rows = p.total_rows;
-  q.rows_a = p.rows_a; q.ga = p.ga; q.gb = p.gb; q.gate = p.gate; q.gate_val = p.gate_val;
+  q.rows_a = p.rows_a; q.ga = p.ga; q.gb = p.gb; q.gate = p.gate; q.gate_val = p.gate_val; q.stall = p.stall;
   q.d = p.d; q.K = p.K; q.nsegs = p.nsegs;
   for (int i = 0; i < p.nsegs; ++i) q.segs[i] = p.segs[i];
   q.combine = p.combine; q.B = p.B; q.residual = p.residual; q.ncomb = p.combine ? p.ncomb : 0; q.flat = p.flat;

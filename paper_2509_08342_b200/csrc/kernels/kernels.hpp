@@ -86,6 +86,7 @@ struct K2Params {
   int ga, gb;
   const unsigned int* gate;
   unsigned int gate_val;
+  unsigned int* stall;    // gated: per-CTA ns spent waiting for the flag (mapped host memory) or nullptr
   int d, K, nsegs;
   int q4;                 // rows are Q4G64 (dequantised on the fly) instead of bf16
   Seg segs[kMaxLaunchSegs];

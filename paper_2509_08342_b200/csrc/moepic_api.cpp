@@ -38,6 +38,7 @@ using namespace moepic;
 namespace {
 
 constexpr int kSMs = 148;
+constexpr int kStallSlot = 160;   // per-CTA gate-wait records per gated K2 launch (>= kSMs)
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
@@ -411,10 +412,24 @@ struct moepic_ctx {
   // gate rarely stalls, and the link idles only for the tail's few rows + the combine.  Without
   // the gate (or when the step does not fit one K2 launch) the tail gets its own launch.
   bool k2_gate = true;
+  bool k2_gate_force = false;   // MOEPIC_K2_GATE=2: gate every decode step, whatever its size
   bool od_tail_auto = true;
   double k2_gate_frac = 0.8;
-  int64_t tail_split_x = 4;   // MOEPIC_TAIL_SPLIT_X
+  int64_t tail_split_x = 2;   // MOEPIC_TAIL_SPLIT_X
   unsigned int gate_seq = 0;
+  // tail-size controller: each gated launch records every CTA's wait at the gate (ns) in mapped
+  // host memory; the next gated step reads the previous launch's mean over the CTAs with gated
+  // rows (that launch finished before this step's router, whose mailbox the host has seen) and
+  // scales the tail: a mean wait over 8 us shrinks it 8 %, under 2 us grows it 3 % -- the tail
+  // lands just after K2 reaches it, so K2 runs under the link and waits only a few us.
+  // MOEPIC_GATE_ADAPT=0: fixed.
+  bool gate_adapt = true;
+  double gate_ctrl = 1.0;
+  unsigned int* stall_h = nullptr;   // [2][kStallSlot] mapped pinned
+  unsigned int* stall_d = nullptr;
+  int stall_slot = 0, stall_prev = -1, stall_prev_g = 0;
+  uint64_t gate_steps = 0;
+  double gate_wait_us_sum = 0.0;
   using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
   WriteValue32Fn write_value32 = nullptr;
   // MOEPIC_TIMELINE=<path> (tools): per decode layer step, %globaltimer stamps of the router, the
@@ -692,9 +707,16 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (const char* e = getenv("MOEPIC_FEED_CHUNK_KB")) ctx->kFeedChunk = (size_t)atol(e) << 10;
   if (const char* e = getenv("MOEPIC_OD_TAIL_MB")) ctx->od_tail_bytes = (size_t)atol(e) << 20, ctx->od_tail_auto = false;
   if (const char* e = getenv("MOEPIC_OD_TAIL_KB")) ctx->od_tail_bytes = (size_t)atol(e) << 10, ctx->od_tail_auto = false;   // tests: small shapes
-  if (const char* e = getenv("MOEPIC_K2_GATE")) ctx->k2_gate = atoi(e) != 0;
+  if (const char* e = getenv("MOEPIC_K2_GATE")) ctx->k2_gate = atoi(e) != 0, ctx->k2_gate_force = atoi(e) == 2;
   if (const char* e = getenv("MOEPIC_K2_GATE_FRAC")) ctx->k2_gate_frac = atof(e);
   if (const char* e = getenv("MOEPIC_TAIL_SPLIT_X")) ctx->tail_split_x = std::max(2L, atol(e));
+  if (const char* e = getenv("MOEPIC_GATE_ADAPT")) ctx->gate_adapt = atoi(e) != 0;
+  if (ctx->k2_gate) {
+    if (cudaHostAlloc(&ctx->stall_h, 2 * kStallSlot * sizeof(unsigned int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->stall_d), ctx->stall_h, 0) != cudaSuccess)
+      return bail(MOEPIC_ENOMEM);
+    memset(ctx->stall_h, 0, 2 * kStallSlot * sizeof(unsigned int));
+  }
   if (ctx->k2_gate) {   // the copy stream's flag write (driver API, resolved through the runtime)
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1039,6 +1061,8 @@ static moepic_status launch_group_tc(moepic_ctx* ctx, const std::vector<StepSeg>
 // Gated launch (K2Gate): segs[0, n_a) are ready at launch, segs[n_a, ...) are the tail of the
 // step's last on-demand copy, streamed by the same launch once the copy stream's flag arrives.
 constexpr size_t kGateOff = 32;   // the copy-stream gate word inside the arena's ticket block
+constexpr double kGateWaitLoUs = 2.0, kGateWaitHiUs = 8.0;   // tail controller: mean wait band
+constexpr uint64_t kGateMinBytes = 256ull << 20;   // gate steps whose K2 rows reach this size
 constexpr double kGateLaunchS = 3e-6;   // K2 ramp (the launch latency is left out: a tail that
                                          // outlasts K2 stalls the gate, measured)
 
@@ -1046,6 +1070,7 @@ struct K2Gate {
   size_t n_a;
   const unsigned int* flag;
   unsigned int val;
+  unsigned int* stall;   // per-CTA wait record (device alias of mapped host memory) or nullptr
 };
 
 // Can one gated K2 launch (with the fused combine) cover these segments?  Needs the CUDA-core K2
@@ -1116,6 +1141,7 @@ static moepic_status launch_group(moepic_ctx* ctx, const std::vector<StepSeg>& s
     kp.gb = (int)GB;
     kp.gate = gate ? gate->flag : nullptr;
     kp.gate_val = gate ? gate->val : 0u;
+    kp.stall = gate ? gate->stall : nullptr;
     kp.h = h;
     kp.ids = reinterpret_cast<const int32_t*>(ctx->arena + ctx->lay.ids);
     kp.w = reinterpret_cast<const float*>(ctx->arena + ctx->lay.w);
@@ -1702,18 +1728,37 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   }
   // gated tail (one K2 launch per step, the last copy's tail streamed after the copy-stream flag)
   const bool q4 = d.weight_format == MOEPIC_Q4G64;
-  const bool gate_mode = ctx->k2_gate && B <= k2_max_tokens(d.d, q4);
+  // gated only where the step's K2 work is large (Mixtral-shaped layers, ~700 MB): there the
+  // single launch matches the split's throughput and cuts the event-timed launch overhead; on
+  // 75-140 MB layers (Qwen3 / DeepSeek shapes) it measured ~2 % slower than the split
+  // (DESIGN.md §6b), so they keep the two launches unless MOEPIC_K2_GATE=2
+  int64_t step_rows_all = (int64_t)res.A.size() * d.I + (int64_t)d.n_shared * (shared_hi(cp) - shared_lo(cp));
+  const bool gate_mode = ctx->k2_gate && B <= k2_max_tokens(d.d, q4) &&
+                         (ctx->k2_gate_force || (uint64_t)step_rows_all * rb >= kGateMinBytes);
   const bool split_ok = B <= kDecodeMaxB && ctx->od_tail_bytes > 0;
   int64_t tail_rows_split = split_ok ? (int64_t)((ctx->od_tail_bytes + rb - 1) / rb) : 0;
+  if (gate_mode && ctx->stall_prev >= 0) {   // the previous gated launch has finished: its waits
+    const unsigned int* rec = ctx->stall_h + (size_t)ctx->stall_prev * kStallSlot;
+    double mean = 0.0;   // over the CTAs that stream gated rows
+    for (int c = 0; c < ctx->stall_prev_g; ++c) mean += rec[c];
+    mean = ctx->stall_prev_g ? mean / ctx->stall_prev_g * 1e-3 : 0.0;   // us
+    ctx->gate_wait_us_sum += mean;
+    ++ctx->gate_steps;
+    if (ctx->gate_adapt) {
+      if (mean > kGateWaitHiUs) ctx->gate_ctrl *= 0.92;
+      else if (mean < kGateWaitLoUs) ctx->gate_ctrl *= 1.03;
+      ctx->gate_ctrl = std::min(8.0, std::max(0.25, ctx->gate_ctrl));
+    }
+    ctx->stall_prev = -1;
+  }
   if (split_ok && gate_mode && ctx->od_tail_auto) {
     // the tail lands while K2 streams the step's other rows: the link stays busy under K2 and the
     // gated rows are streamed as they land.  Tail = k2_gate_frac x (K2 time of the step's rows +
     // ~3 us ramp) at the link rate (K2 ~6 TB/s on bf16 rows, ~1.6 TB/s dequantising
     // Q4G64; link ~55 GB/s, both measured); below 1 so that the gate itself rarely waits
-    int64_t step_rows = (int64_t)res.A.size() * d.I;
-    step_rows += (int64_t)d.n_shared * (shared_hi(cp) - shared_lo(cp));
+    const int64_t step_rows = step_rows_all;
     const double k2_s = (double)step_rows * rb / (q4 ? 1.6e12 : 6.0e12) + kGateLaunchS;
-    tail_rows_split = std::max<int64_t>(1, (int64_t)(ctx->k2_gate_frac * k2_s * 55e9 / rb));
+    tail_rows_split = std::max<int64_t>(1, (int64_t)(ctx->k2_gate_frac * ctx->gate_ctrl * k2_s * 55e9 / rb));
   }
   // a copy is split only when it is well above the tail (split_x x tail): every extra DMA costs
   // ~4 us of link time (scripts/dma_probe.cu), a somewhat long whole-copy tail only a short wait
@@ -1798,24 +1843,6 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
   }
   std::vector<uint32_t> masks(res.A.size());
   std::vector<uint8_t*> od_rest(d.N, nullptr);   // gamma with a prefetched prefix: where row `prefix` lands
-  // gated tail: the step's last copy should be a small one -- a bottom rather than a gamma top
-  // (I_top rows) -- so that it can be the tail whole, without an extra DMA.  With gamma tops to
-  // copy in pass 2, the last pass-1 bottom is held back and issued after them (the link is busy
-  // with the copies before it meanwhile).
-  int defer_a = -1;
-  if (gate_mode && split_ok && ctx->od_tail_auto && l.I_top > 0) {
-    bool pass2 = false;
-    for (size_t a = 0; a < res.A.size(); ++a)
-      if (res.cls[a] == kGamma && res.plan_idx[a] < 0) pass2 = true;
-    int n1 = 0;   // pass-1 bottoms: hold one back only if another keeps the link busy meanwhile
-    if (pass2)
-      for (size_t a = 0; a < res.A.size(); ++a)
-        if (res.plan_idx[a] < 0 && (res.cls[a] == kBeta || (res.cls[a] == kGamma && l.I_top < d.I))) {
-          defer_a = (int)a;
-          ++n1;
-        }
-    if (n1 < 2) defer_a = -1;
-  }
   for (size_t a = 0; a < res.A.size(); ++a) {   // pass 1: everything classification decides
     const int e = res.A[a];
     const uint32_t m = masks[a] = mask_of(e);
@@ -1835,7 +1862,7 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
         gC.push_back(StepSeg{dst, e, rows, m, r0});
         od_row += rows;
       }
-    } else if ((c == kBeta || (c == kGamma && l.I_top < d.I)) && (int)a != defer_a) {
+    } else if (c == kBeta || (c == kGamma && l.I_top < d.I)) {
       // missing bottom rows [I_top, I): known from classification alone (a gamma expert's top
       // rows follow in pass 2, once admission has chosen their destination)
       const int rows = d.I - l.I_top;
@@ -1873,15 +1900,6 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     }
     if ((st = copy(top, ctx->host_expert(layer, e), l.I_top, slot >= 0)) != MOEPIC_OK) return st;
     gC.push_back(StepSeg{top, e, l.I_top, masks[a], 0});
-  }
-  if (defer_a >= 0) {   // the held-back bottom: the step's last copy
-    const int e = res.A[defer_a];
-    const int rows = d.I - l.I_top;
-    uint8_t* dst = ctx->od_ptr(buf, od_row);
-    if ((uint64_t)(od_row + rows) > ctx->lay.od_rows) return ctx->poisoned = true, fail(&ctx->err, MOEPIC_ERUNTIME, "on-demand region overflow");
-    if ((st = copy(dst, ctx->host_expert(layer, e) + (uint64_t)l.I_top * rb, rows)) != MOEPIC_OK) return st;
-    gC.push_back(StepSeg{dst, e, rows, masks[defer_a], l.I_top});
-    od_row += rows;
   }
   // the split copy's segment is the last one pushed to gC: cut its tail into its own segment
   const uint8_t* tail_base = nullptr;
@@ -1946,8 +1964,16 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     CK(cudaStreamWaitEvent(s, ctx->ev_od_head, 0));
     if (gated && tail[0].mask != 0 && k2_gate_feasible(ctx, first.size() + 1, B)) {
       // ONE launch: everything but the tail now, the tail behind the copy-stream flag
+      unsigned int* srec = nullptr;
+      if (ctx->stall_h) {   // this launch's wait record: zeroed, read back at the next gated step
+        memset(ctx->stall_h + (size_t)ctx->stall_slot * kStallSlot, 0, kStallSlot * sizeof(unsigned int));
+        srec = ctx->stall_d + (size_t)ctx->stall_slot * kStallSlot;
+        ctx->stall_prev = ctx->stall_slot;
+        ctx->stall_prev_g = (int)std::min<int64_t>(kSMs, tail[0].nrows);   // CTAs with gated rows (GB)
+        ctx->stall_slot ^= 1;
+      }
       const K2Gate gate{first.size(), reinterpret_cast<const unsigned int*>(ctx->arena + ctx->lay.ticket + kGateOff),
-                        ctx->gate_seq};
+                        ctx->gate_seq, srec};
       std::vector<StepSeg> all(first);
       all.push_back(tail[0]);
       st = launch_group(ctx, all, h, B, s, ws_next, comb, launches, &fuse, &gate);
@@ -2663,6 +2689,9 @@ void moepic_destroy(moepic_ctx* ctx) {
   if (ctx->hc_n)
     fprintf(stderr, "[hosttiming] %llu copies: stream waits %.1f us, cudaMemcpyAsync %.1f us per copy\n",
             (unsigned long long)ctx->hc_n, ctx->hc[0] / ctx->hc_n, ctx->hc[1] / ctx->hc_n);
+  if (ctx->gate_steps && ctx->host_timing)
+    fprintf(stderr, "[hosttiming] gated K2: %llu steps, mean max gate wait %.1f us, tail controller %.3f\n",
+            (unsigned long long)ctx->gate_steps, ctx->gate_wait_us_sum / ctx->gate_steps, ctx->gate_ctrl);
   if (ctx->k1dbg) {   // MOEPIC_K1_TRACE summary: mean phase offsets from the first CTA start (us)
     std::vector<unsigned long long> h(4096 * 8);
     cudaMemcpy(h.data(), ctx->k1dbg, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -2704,6 +2733,7 @@ void moepic_destroy(moepic_ctx* ctx) {
   if (ctx->host_experts) cudaFreeHost(ctx->host_experts);
   if (ctx->mailbox) cudaFreeHost(ctx->mailbox);
   if (ctx->scratch_h) cudaFreeHost(ctx->scratch_h);
+  if (ctx->stall_h) cudaFreeHost(ctx->stall_h);
   delete ctx;
 }
 

@@ -1,6 +1,7 @@
 """GPU parity of the gated K2 launch (MOEPIC_K2_GATE).
 
-With the gate (default) a decode step issues ONE K2 launch: the resident, prefetched and landed
+With the gate (default on steps with >= 256 MB of K2 rows, MOEPIC_K2_GATE=2 on every step, as
+here on small shapes) a decode step issues ONE K2 launch: the resident, prefetched and landed
 on-demand rows now, and the tail of the step's last on-demand copy once the copy stream's flag
 (written after that copy) arrives.  The gate changes when rows are streamed, never which rows or
 how they are summed per (segment, CTA) partial -- so the traces are the oracle's bit for bit and y
@@ -103,7 +104,7 @@ def test_gate_parity_vs_oracle_and_ungated(dims, B, v_e, q4, env, monkeypatch):
     H = synth.hidden_states(12, 4 * B, L, d)
     toks = [[H[t * B:(t + 1) * B, i] for i in range(L)] for t in range(4)]
     cfg = dict(v_e=v_e, seed=3)
-    y_g, l_g = _run(m, B, cfg, toks, q4=q4, env=env, monkeypatch=monkeypatch)
+    y_g, l_g = _run(m, B, cfg, toks, q4=q4, env={**env, "MOEPIC_K2_GATE": "2"}, monkeypatch=monkeypatch)
     y_u, l_u = _run(m, B, cfg, toks, q4=q4, env={**env, "MOEPIC_K2_GATE": "0"}, monkeypatch=monkeypatch)
     for a, b in zip(y_g, y_u):
         assert rel_err(a, b) <= 1e-5
@@ -119,7 +120,7 @@ def test_gate_single_small_copy_is_the_tail(monkeypatch):
     H = synth.hidden_states(5, 8, 2, S.d)
     toks = [[H[t, i][None] for i in range(2)] for t in range(8)]
     cfg = dict(v_e=4.0, theta_i=[1.0, 1.0], seed=0)
-    y_g, l_g = _run(m, 1, cfg, toks, env={}, monkeypatch=monkeypatch, g=16)
+    y_g, l_g = _run(m, 1, cfg, toks, env={"MOEPIC_K2_GATE": "2"}, monkeypatch=monkeypatch, g=16)
     y_u, l_u = _run(m, 1, cfg, toks, env={"MOEPIC_K2_GATE": "0"}, monkeypatch=monkeypatch, g=16)
     for a, b in zip(y_g, y_u):
         assert rel_err(a, b) <= 1e-5
