@@ -398,17 +398,28 @@ def run_ours(args, log):
         # at that many rows of link time.  The configuration is solved again on the statistics
         # of the adaptation tokens alone (snapshot restored), so the window is the only change;
         # it is not fed to Alg. 1 as T_att (that moved DeepSeek to smaller theta, -3.5 %).
-        cc0 = ctx.counters()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
+        # per token: (token time - its PCIe bytes / link rate) / L; the median over the tokens, so
+        # one slow token (a host hiccup) cannot switch the window on (a mean once read 738 us on
+        # a Mixtral stack whose idle is ~65 us per layer)
+        marks = []   # (events, PCIe bytes) per token; the counters are host-side, no sync needed
         for t in range(warm_tokens, pre_tokens):
+            cc0 = ctx.counters()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
             step(t)
-        a1.record(stream)
+            a1.record(stream)
+            cc1 = ctx.counters()
+            marks.append((a0, a1, cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] -
+                          cc0["pcie_ondemand_bytes"] - cc0["pcie_prefetch_bytes"]))
         torch.cuda.synchronize()
-        cc1 = ctx.counters()
-        lay_ms = a0.elapsed_time(a1) / (cal_tokens * L)
-        link_ms = (cc1["pcie_ondemand_bytes"] + cc1["pcie_prefetch_bytes"] - cc0["pcie_ondemand_bytes"]
-                   - cc0["pcie_prefetch_bytes"]) / (cal_tokens * L) / (ALG1_PCIE_GBS * 1e9) * 1e3
+        per_tok_idle = []
+        for a0, a1, nbytes in marks:
+            tok_ms = a0.elapsed_time(a1)
+            tok_link_ms = nbytes / (ALG1_PCIE_GBS * 1e9) * 1e3
+            per_tok_idle.append(((tok_ms - tok_link_ms) / L, tok_ms / L))
+        per_tok_idle.sort()
+        idle_ms_med, lay_ms = per_tok_idle[len(per_tok_idle) // 2]
+        link_ms = lay_ms - idle_ms_med
         # three quarters of it: the next layer's on-demand copies queue behind the prefetch (one
         # FIFO copy stream), so the window leaves their DMA start-up its own margin
         idle_us = (lay_ms - link_ms) * 1e3
