@@ -209,7 +209,11 @@ moepic_status moepic_configure(moepic_ctx* ctx, const moepic_cache_config* cfg,
  *   stream: cudaStream_t (as void*; NULL = legacy default stream) all compute is ordered on.
  *   trace: may be NULL.
  * Blocks the host only until the routing of this batch is known (it plans copies); returns
- * with the GPU work enqueued on `stream`.  y_dev is valid after the stream reaches it.        */
+ * with the GPU work enqueued on `stream`.  y_dev is valid after the stream reaches it.
+ * Schedule (decode): on-demand copies on the context's copy stream; the split-
+ * expert kernel covers the resident, prefetched and landed rows, and the tail of the last copy
+ * either in the same launch behind a copy-stream flag (steps with >= 256 MB of rows;
+ * MOEPIC_K2_GATE=0 never, =2 always) or in a second launch.  Results do not depend on it.     */
 moepic_status moepic_layer_forward(moepic_ctx* ctx, int32_t layer, const void* h_dev, int32_t B,
                                    float* y_dev, void* stream, uint32_t flags,
                                    moepic_trace* trace);
