@@ -24,8 +24,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, B, fmt=0):
+def _worker(rank, world, port, q, B, fmt=0, gate=1):
     try:
+        os.environ["MOEPIC_K2_GATE"] = str(gate)   # read at create
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -75,14 +76,15 @@ def _worker(rank, world, port, q, B, fmt=0):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B,fmt", [(1, 0), (3, 0), (64, 0), (3, 1)])
-def test_ep_two_ranks_one_gpu(B, fmt):
+@pytest.mark.parametrize("B,fmt,gate", [(1, 0, 1), (3, 0, 1), (64, 0, 1), (3, 1, 1), (1, 0, 2), (3, 0, 2)])
+def test_ep_two_ranks_one_gpu(B, fmt, gate):
+    """gate 2: every decode step runs the gated K2 launch (MOEPIC_K2_GATE=2)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, B, fmt)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, B, fmt, gate)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=600) for _ in ps)

@@ -33,6 +33,9 @@ def _free_port():
 
 def _worker(rank, world, port, q, mode, B, transport):
     try:
+        if mode.endswith("+gate"):   # every decode step on the gated K2 launch
+            os.environ["MOEPIC_K2_GATE"] = "2"
+            mode = mode[:-5]
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -116,7 +119,8 @@ def _run(mode, B, transport=0, timeout=600):
     return res
 
 
-@pytest.mark.parametrize("mode,B", [("ep", 1), ("ep", 3), ("tp", 2), ("sharded", 3), ("sharded", 40)])
+@pytest.mark.parametrize("mode,B", [("ep", 1), ("ep", 3), ("tp", 2), ("sharded", 3), ("sharded", 40),
+                                    ("ep+gate", 1), ("tp+gate", 2)])
 def test_group_peer_two_ranks_one_gpu(mode, B):
     res = _run(mode, B)
     assert res == {0: "ok", 1: "ok"}, res
