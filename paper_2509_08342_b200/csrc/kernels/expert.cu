@@ -127,14 +127,13 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   // ------------------------------------------------------------------ TMA producer (warp 0 lane 0)
   // Prologue fills every stage; afterwards tile n-1+S is issued into tile n-1's stage as soon as
   // all warps released it (in iteration n, right after warp 0's own release).  The producer walks
-  // the CTA's phase-0 rows, then its gated rows.
+  // the CTA's phase-0 rows with the phase-0 loop (range end loop-invariant, as with one range);
+  // the gated rows are issued by the gated loop itself, after the copy-stream flag (the ring has
+  // drained by then: one TMA round trip per launch).
   const bool producer = tid == 0;
   uint64_t pol = 0;
   Tile pit;
-  int64_t plim;
-  bool pgated;
-  if (a0 < a1) pit.s = sA, pit.row = a0, plim = a1, pgated = false;
-  else pit.s = sB, pit.row = b0, plim = b1, pgated = true;
+  pit.s = sA, pit.row = a0;
   int pn = 0;   // next tile index to issue
   // wait for the copy-stream flag; the CTA's wait (ns) feeds the host's tail-size controller
   auto gate_pass = [&]() {
@@ -146,32 +145,21 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       p.stall[blockIdx.x] = w > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned int)w;
     }
   };
-  auto issue = [&]() {
+  auto issue = [&](int64_t lim) {
     const int pst = pn % kStagesV2;
-    const int64_t e = tile_end(pit, plim);
+    const int64_t e = tile_end(pit, lim);
     const Seg& sg = p.segs[pit.s];
     const uint32_t bytes = (uint32_t)((e - pit.row) * rowb);
     mbar_expect_tx(&full[pst], bytes);
     bulk_g2s(stages + (size_t)pst * tileb, sg.base + (pit.row - sg.row_begin) * rowb, bytes, &full[pst], pol);
-    advance(pit, plim);
+    advance(pit, lim);
     ++pn;
-  };
-  // is there a tile to issue?  Once the phase-0 rows are issued, switch to the gated rows and wait
-  // (once) for the copy-stream flag: warp 0 waits with it, the tiles already in the ring complete
-  // on their own and are consumed once the flag is seen
-  auto more = [&]() -> bool {
-    if (pit.row < plim) return true;
-    if (pgated) return false;
-    pit.s = sB, pit.row = b0, plim = b1, pgated = true;
-    if (pit.row >= plim) return false;
-    if (p.gate) gate_pass();
-    return true;
   };
   if (producer) {
     pol = evict_first_policy();
-    if (pgated && p.gate) gate_pass();   // a CTA with gated rows only
-    while (pn < kStagesV2 && more()) issue();
+    while (pn < kStagesV2 && pit.row < a1) issue(a1);
   }
+  bool b_started = false;
 
   // ------------------------------------------------------------------ consumer warps
   const int c0 = tid * CW;               // first owned column
@@ -286,12 +274,23 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
   int n = 0;
   // the CTA's phase-0 rows, then its gated rows: the same loop body instantiated for each range
   // (a loop-invariant range end keeps the tile walk in the uniform datapath, as with one range)
-  auto run_range = [&](const int64_t r0, const int64_t r1, const int s0) {
+  auto run_range = [&](const int64_t r0, const int64_t r1, const int s0, const bool is_b) {
   Tile it;
   it.s = s0;
   it.row = r0;
   for (; it.row < r1; ++n) {
     const int st = n % kStagesV2;
+    if (is_b && producer) {   // gated rows: the flag once, then the tile this iteration needs
+      if (!b_started) {
+        if (p.gate) gate_pass();
+        pit.s = sB, pit.row = b0;
+        b_started = true;
+      }
+      while (pn <= n && pit.row < r1) {   // tile pn's stage: tile pn-S, released iterations ago
+        if (pn >= kStagesV2) mbar_wait(&empty[pn % kStagesV2], (pn / kStagesV2 - 1) & 1);
+        issue(r1);
+      }
+    }
     const int s = it.s;
     const int nr = (int)(tile_end(it, r1) - it.row);
     if (s != cur) {                      // new segment: its tokens, weights and h columns
@@ -415,9 +414,16 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
       phase2();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[prev_stage]);
-      if (producer && more()) {   // refill tile n-1's stage with tile n-1+S
-        mbar_wait(&empty[prev_stage], ((n - 1) / kStagesV2) & 1);
-        issue();
+      if (!is_b) {
+        if (producer && pit.row < r1) {   // refill tile n-1's stage with tile n-1+S
+          mbar_wait(&empty[prev_stage], ((n - 1) / kStagesV2) & 1);
+          issue(r1);
+        }
+      } else if (producer) {   // gated rows: up to S tiles ahead (every tile <= n-1 released now)
+        while (pn <= n - 1 + kStagesV2 && pit.row < r1) {
+          mbar_wait(&empty[pn % kStagesV2], (pn / kStagesV2 - 1) & 1);
+          issue(r1);
+        }
       }
       if (prev_seg != s) flush(prev_seg, prev_ntok);
     }
@@ -458,8 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1) k2_split_expert(const __grid_cons
     advance(it, r1);
   }
   };
-  run_range(a0, a1, sA);
-  run_range(b0, b1, sB);
+  run_range(a0, a1, sA, false);
+  run_range(b0, b1, sB, true);
   if (prev_stage >= 0) {
     phase2();
     flush(prev_seg, prev_ntok);
