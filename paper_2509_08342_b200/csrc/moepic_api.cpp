@@ -425,6 +425,7 @@ struct moepic_ctx {
   // MOEPIC_GATE_ADAPT=0: fixed.
   bool gate_adapt = true;
   double gate_ctrl = 1.0;
+  double gate_wait_lo_us = 2.0, gate_wait_hi_us = 8.0;   // mean-wait band (MOEPIC_GATE_WAIT_US=lo,hi)
   unsigned int* stall_h = nullptr;   // [2][kStallSlot] mapped pinned
   unsigned int* stall_d = nullptr;
   int stall_slot = 0, stall_prev = -1, stall_prev_g = 0;
@@ -711,6 +712,10 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (const char* e = getenv("MOEPIC_K2_GATE_FRAC")) ctx->k2_gate_frac = atof(e);
   if (const char* e = getenv("MOEPIC_TAIL_SPLIT_X")) ctx->tail_split_x = std::max(2L, atol(e));
   if (const char* e = getenv("MOEPIC_GATE_ADAPT")) ctx->gate_adapt = atoi(e) != 0;
+  if (const char* e = getenv("MOEPIC_GATE_WAIT_US")) {
+    double lo = 0, hi = 0;
+    if (sscanf(e, "%lf,%lf", &lo, &hi) == 2 && lo >= 0 && hi > lo) ctx->gate_wait_lo_us = lo, ctx->gate_wait_hi_us = hi;
+  }
   if (ctx->k2_gate) {
     if (cudaHostAlloc(&ctx->stall_h, 2 * kStallSlot * sizeof(unsigned int), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->stall_d), ctx->stall_h, 0) != cudaSuccess)
@@ -1061,7 +1066,6 @@ static moepic_status launch_group_tc(moepic_ctx* ctx, const std::vector<StepSeg>
 // Gated launch (K2Gate): segs[0, n_a) are ready at launch, segs[n_a, ...) are the tail of the
 // step's last on-demand copy, streamed by the same launch once the copy stream's flag arrives.
 constexpr size_t kGateOff = 32;   // the copy-stream gate word inside the arena's ticket block
-constexpr double kGateWaitLoUs = 2.0, kGateWaitHiUs = 8.0;   // tail controller: mean wait band
 constexpr uint64_t kGateMinBytes = 256ull << 20;   // gate steps whose K2 rows reach this size
 constexpr double kGateLaunchS = 3e-6;   // K2 ramp (the launch latency is left out: a tail that
                                          // outlasts K2 stalls the gate, measured)
@@ -1745,8 +1749,8 @@ static moepic_status layer_forward_impl(moepic_ctx* ctx, int32_t layer, const vo
     ctx->gate_wait_us_sum += mean;
     ++ctx->gate_steps;
     if (ctx->gate_adapt) {
-      if (mean > kGateWaitHiUs) ctx->gate_ctrl *= 0.92;
-      else if (mean < kGateWaitLoUs) ctx->gate_ctrl *= 1.03;
+      if (mean > ctx->gate_wait_hi_us) ctx->gate_ctrl *= 0.92;
+      else if (mean < ctx->gate_wait_lo_us) ctx->gate_ctrl *= 1.03;
       ctx->gate_ctrl = std::min(8.0, std::max(0.25, ctx->gate_ctrl));
     }
     ctx->stall_prev = -1;
