@@ -1,7 +1,7 @@
 """NEXT-1 ablations on the same engine: run bench.py once per (config, mode) and
 write a markdown table of decode throughput, per-layer latency, PCIe bytes and hit rates.
 
-    python scripts/ablation.py [--configs mixtral qwen3 deepseek] [--steps 8] [--out profiles/r01_ablation.md]
+    python scripts/ablation.py [--configs mixtral qwen3 deepseek] [--steps 32] [--out profiles/r02_ablation.md]
 """
 import argparse
 import json
@@ -19,7 +19,7 @@ def main():
     ap.add_argument("--configs", nargs="+", default=["mixtral", "qwen3", "deepseek"])
     ap.add_argument("--modes", nargs="+", default=list(MODES))
     ap.add_argument("--steps", type=int, default=8)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_ablation.md"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_ablation.md"))
     ap.add_argument("--jsonl", default=os.path.join(ROOT, "gpurun_out", "ablation.jsonl"))
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.jsonl), exist_ok=True)
