@@ -412,6 +412,7 @@ struct moepic_ctx {
   // gate rarely stalls, and the link idles only for the tail's few rows + the combine.  Without
   // the gate (or when the step does not fit one K2 launch) the tail gets its own launch.
   bool k2_gate = true;
+  bool pf_merge_ab = true;      // prefill: resident + prefetched segments in one GEMM group (MOEPIC_PF_MERGE_AB)
   bool k2_gate_force = false;   // MOEPIC_K2_GATE=2: gate every decode step, whatever its size
   bool od_tail_auto = true;
   double k2_gate_frac = 0.8;
@@ -710,6 +711,7 @@ moepic_status moepic_create(const moepic_model_desc* desc, void* dev_arena, size
   if (const char* e = getenv("MOEPIC_OD_TAIL_KB")) ctx->od_tail_bytes = (size_t)atol(e) << 10, ctx->od_tail_auto = false;   // tests: small shapes
   if (const char* e = getenv("MOEPIC_K2_GATE")) ctx->k2_gate = atoi(e) != 0, ctx->k2_gate_force = atoi(e) == 2;
   if (const char* e = getenv("MOEPIC_K2_GATE_FRAC")) ctx->k2_gate_frac = atof(e);
+  if (const char* e = getenv("MOEPIC_PF_MERGE_AB")) ctx->pf_merge_ab = atoi(e) != 0;
   if (const char* e = getenv("MOEPIC_TAIL_SPLIT_X")) ctx->tail_split_x = std::max(2L, atol(e));
   if (const char* e = getenv("MOEPIC_GATE_ADAPT")) ctx->gate_adapt = atoi(e) != 0;
   if (const char* e = getenv("MOEPIC_GATE_WAIT_US")) {
@@ -1614,11 +1616,25 @@ static moepic_status prefill_launch(moepic_ctx* ctx, const uint16_t* h, int T, f
     }
     return MOEPIC_OK;
   };
-  moepic_status st = run_group(gA);
-  if (st != MOEPIC_OK) return st;
-  if (!gB.empty()) {
+  // resident tops and prefetched rows as ONE group once the plan has landed (it was issued a layer
+  // earlier, behind that layer's on-demand copies): two GEMM launches fewer per layer, and the
+  // resident GEMMs still run while this layer's on-demand copies stream.  An expert's segments
+  // stay consecutive, top first (the down GEMM groups by expert).
+  moepic_status st;
+  if (!gB.empty() && ctx->pf_merge_ab) {
+    std::vector<StepSeg> gAB(gA);
+    gAB.insert(gAB.end(), gB.begin(), gB.end());
+    std::stable_sort(gAB.begin(), gAB.end(), [](const StepSeg& x, const StepSeg& y) {
+      return x.expert != y.expert ? x.expert < y.expert : x.row0 < y.row0;
+    });
     CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
-    if ((st = run_group(gB)) != MOEPIC_OK) return st;
+    if ((st = run_group(gAB)) != MOEPIC_OK) return st;
+  } else {
+    if ((st = run_group(gA)) != MOEPIC_OK) return st;
+    if (!gB.empty()) {
+      CK(cudaStreamWaitEvent(s, ctx->ev_plan[buf], 0));
+      if ((st = run_group(gB)) != MOEPIC_OK) return st;
+    }
   }
   if (!gC.empty()) {
     CK(cudaStreamWaitEvent(s, ctx->ev_od, 0));
